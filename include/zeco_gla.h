@@ -1,0 +1,134 @@
+/*
+ * zeco_gla.h -- C ABI of the B200-native ZeCO sequence-parallel GLA library
+ * (libzeco_gla.so).  Plain pointers and sizes only; every compute entry point
+ * is stream-ordered on a CUDA stream passed as `void*` (0 = legacy default)
+ * and takes DEVICE pointers owned by the caller.  Return value: ZGLA_OK (0)
+ * or a negative ZGLA_ERR_* code; the Python drop-in maps the codes onto the
+ * reference exception types (glasp/errors.py:4-33).
+ *
+ * The reference (`glasp`, pure Python/NumPy) has no FFI; each entry point
+ * below names the reference function it replaces.  INTEGRATION.md shows the
+ * ctypes binding the reference would add.
+ *
+ * Layouts (reference glasp/gla.py:29-30): q,k,g [h][L][dk], v,o [h][L][dv],
+ * contiguous.  States are [h][dk][dv]; lists of N+1 boundary states are
+ * stacked as [N+1][h][dk][dv]; cumulative log decays as [N+1][h][dk].
+ *
+ * Precision modes (zgla_dtype):
+ *   ZGLA_BF16: q,k,v,dO,o,dq,dk,dv are bf16; g, dg, states are fp32.  ZeCO
+ *              entry points use the tcgen05/TMEM/TMA kernels when
+ *              dk,dv in {64,128} and L % 64 == 0.
+ *   ZGLA_F32 : everything fp32 ("fp32 validation mode", SIMT FMA kernels).
+ *   ZGLA_F64 : everything fp64 (bit-for-bit reference semantics for tests).
+ */
+#ifndef ZECO_GLA_H
+#define ZECO_GLA_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZGLA_OK 0
+#define ZGLA_ERR_DIMS (-1)        /* -> DimsError   */
+#define ZGLA_ERR_DOMAIN (-2)      /* -> DomainError */
+#define ZGLA_ERR_LAYOUT (-3)      /* -> LayoutError */
+#define ZGLA_ERR_CONFIG (-4)      /* -> ConfigError */
+#define ZGLA_ERR_STATE (-5)       /* -> StateError  */
+#define ZGLA_ERR_DEADLOCK (-6)    /* -> DeadlockError (All-Scan flag wait timed out) */
+#define ZGLA_ERR_UNSUPPORTED (-7) /* shape not supported by this build */
+#define ZGLA_ERR_CUDA (-100)      /* CUDA runtime error; see zgla_last_error() */
+
+enum { ZGLA_BF16 = 0, ZGLA_F32 = 1, ZGLA_F64 = 2 };
+enum { ZGLA_FWD = 0, ZGLA_BWD = 1 };
+
+typedef struct {
+  int heads;
+  int key_dim;
+  int value_dim;
+  int chunk_len;
+  long long seq_len; /* tokens in this shard */
+  int dtype;         /* ZGLA_BF16 / ZGLA_F32 / ZGLA_F64 */
+} zgla_shape;
+
+/* ---- library ----------------------------------------------------------- */
+const char* zgla_version(void);
+const char* zgla_last_error(void);
+/* 1 if the fused tcgen05 ZeCO kernels serve this shape, else 0 */
+int zgla_fast_path(const zgla_shape* s);
+
+/* ---- reference function-level API (glasp/gla.py) ------------------------ */
+/* bytes of device workspace the function-level entry points below need */
+long long zgla_workspace_bytes(const zgla_shape* s);
+
+/* glasp/gla.py:248 local_state_scan (+ optional initial state, glasp/gla.py:210 init) */
+int zgla_local_state_scan(const zgla_shape* s, const void* k, const void* v, const void* g, const void* init,
+                          void* states_out, void* cum_out, void* ws, void* stream);
+/* glasp/gla.py:297 forward_outputs; prev may be NULL (zero state) */
+int zgla_forward_outputs(const zgla_shape* s, const void* q, const void* k, const void* v, const void* g,
+                         const void* states, const void* cum, const void* prev, void* o, void* stream);
+/* glasp/gla.py:272 global_correct over n_states boundary states */
+int zgla_global_correct(const zgla_shape* s, int n_states, const void* states, const void* cum, const void* prev,
+                        void* out, void* stream);
+/* glasp/gla.py:336 reverse_boundary_scan; seed may be NULL (zero) */
+int zgla_reverse_boundary_scan(const zgla_shape* s, const void* q, const void* g, const void* d_out,
+                               const void* seed, void* rev_out, void* ws, void* stream);
+/* glasp/gla.py:359 backward; saved_states may be NULL (recompute from prev) */
+int zgla_backward(const zgla_shape* s, const void* q, const void* k, const void* v, const void* g,
+                  const void* d_out, const void* prev, const void* ds_next, const void* saved_states, void* dq,
+                  void* dk, void* dv, void* dg, void* ds_boundary, void* ws, void* stream);
+/* glasp/gla.py:331 revcum along tokens of an [h][L][d] tensor (acc dtype of s) */
+int zgla_revcum(const zgla_shape* s, int d, const void* x, void* out, void* stream);
+/* glasp/gla.py:233 chunk_scalings of one chunk g [h][C][dk] */
+int zgla_chunk_scalings(const zgla_shape* s, const void* g_chunk, void* chunk_decay, void* from_start,
+                        void* to_end, void* stream);
+/* elementwise domain checks used by SeqShard/State validation; *bad set to 1 if violated */
+int zgla_check_log_decay(long long n, int dtype, const void* g, int* bad_dev, void* stream);
+
+/* ---- ZeCO per-rank hot path (glasp/engine.py:218-237, 348-364) --------- */
+/* plan-dependent workspace for the four ZeCO entry points */
+long long zgla_zeco_workspace_bytes(const zgla_shape* s, int num_sms);
+/* local chunk scan: rank-local final state S_local [h][dk][dv] and total log decay G_tot [h][dk]
+ * (glasp/engine.py:219-224 -> inputs of All-Scan FWD) */
+int zgla_zeco_fwd_local(const zgla_shape* s, int num_sms, const void* k, const void* v, const void* g, void* ws,
+                        void* s_local, void* g_tot, void* stream);
+/* outputs with the fused correction O += (Q e^{G_t}) S_prev; s_prev may be NULL (rank 0) */
+int zgla_zeco_fwd_output(const zgla_shape* s, int num_sms, const void* q, const void* k, const void* v,
+                         const void* g, void* ws, const void* s_prev, void* o, void* stream);
+/* local reverse scan: dS_local0 [h][dk][dv] (input of All-Scan BWD, glasp/engine.py:349-355) */
+int zgla_zeco_bwd_local(const zgla_shape* s, int num_sms, const void* q, const void* g, const void* d_out,
+                        void* ws, void* ds_local0, void* stream);
+/* gradients with the fused corrections from s_prev / ds_next (either may be NULL) */
+int zgla_zeco_bwd_output(const zgla_shape* s, int num_sms, const void* q, const void* k, const void* v,
+                         const void* g, const void* d_out, void* ws, const void* s_prev, const void* ds_next,
+                         void* dq, void* dk, void* dv, void* dg, void* stream);
+
+/* ---- All-Scan (glasp/collectives.py:70-140) ----------------------------- */
+/* All P "ranks" resident on one device (the reference's list form): one kernel runs the
+ * whole pipelined chain through device-memory flags.  fp32 or fp64 (dtype). */
+int zgla_allscan_local(int P, int heads, int key_dim, int value_dim, int dtype, int num_blocks, int direction,
+                       const void* local_states, const void* log_decays, void* recv, void* scanned,
+                       void* stream);
+
+/* SPMD form over peer memory (one process per GPU).  The caller exchanges the
+ * buffers returned by zgla_allscan_export() (CUDA IPC handles) and passes the
+ * successor/predecessor mappings to zgla_allscan_bind(). */
+typedef struct zgla_allscan_comm zgla_allscan_comm;
+int zgla_allscan_create(int rank, int world, int heads, int key_dim, int value_dim, int max_blocks,
+                        zgla_allscan_comm** out);
+int zgla_allscan_export(zgla_allscan_comm* c, void* ipc_handle_out /* 64 bytes */);
+int zgla_allscan_bind(zgla_allscan_comm* c, const void* next_handle, const void* prev_handle);
+/* bind to buffers in this process (world of virtual ranks inside one process) */
+int zgla_allscan_bind_local(zgla_allscan_comm* c, zgla_allscan_comm* next, zgla_allscan_comm* prev);
+int zgla_allscan_run(zgla_allscan_comm* c, int num_blocks, int direction, const float* local_state,
+                     const float* log_decay, float* recv, float* scanned, void* stream);
+int zgla_allscan_destroy(zgla_allscan_comm* c);
+long long zgla_allscan_bytes_sent(const zgla_allscan_comm* c);
+
+/* ---- diagnostics -------------------------------------------------------- */
+int zgla_selftest_mma(const void* a, const void* b, float* d, int M, int N, int K, int a_mn, int b_mn,
+                      int lane_off, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZECO_GLA_H */

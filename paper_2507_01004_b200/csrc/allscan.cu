@@ -1,0 +1,359 @@
+// All-Scan (paper Alg. 2; reference glasp/collectives.py:70-140) as an in-kernel
+// pipelined chain over peer memory.
+//
+// Every rank owns, per direction, an INBOX (one state, fp32 [h][dk][dv]), a
+// FLAGS array and an ACK array ([K pipeline blocks][B CTAs] u32 each).  Rank
+// p's kernel, for every pipeline block b (rows [b*dk/K, (b+1)*dk/K) of all
+// heads) and for its slice of that block:
+//   1. waits until FLAGS[b][cta] >= epoch (predecessor's data has landed),
+//   2. computes  scanned = e^{G_p} (.) recv + local  (recv = inbox, 0 at the source),
+//   3. stores scanned straight into the SUCCESSOR's inbox (NVLink P2P store
+//      when the successor is another GPU) and, after a system-scope fence,
+//      publishes FLAGS[b][cta] = epoch in the successor's memory,
+//   4. acks consumption of its own inbox block to the predecessor.
+// A producer only overwrites a successor inbox block once that block's ACK
+// from the previous epoch has arrived, so back-to-back calls are safe.  Blocks
+// pipeline exactly as in the reference: rank p forwards block b while block
+// b+1 is still in flight, giving the (K+P-1) hop schedule of Eq. 13.
+//
+// The same device code runs the reference's list form (all P ranks resident on
+// one GPU, zgla_allscan_local / zgla_allscan_bind_local) and the SPMD form
+// (one process per GPU, peers mapped with CUDA IPC).  Results are elementwise
+// and independent of K and of the CTA split, so they are bit-identical for
+// every K (reference tests/test_collectives.py:88-103).
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "zgla_internal.h"
+
+namespace zgla {
+namespace allscan {
+
+constexpr int kThreads = 256;
+constexpr int kCtasPerRank = 8;
+
+template <typename T>
+struct Link {
+  const T* local;
+  const T* logdecay;
+  const T* inbox;         // my incoming buffer (nullptr at the source)
+  const unsigned* flags;  // my incoming flags
+  unsigned* ack_to_pred;  // predecessor's ACK array (peer), nullptr at the source
+  T* succ_inbox;          // successor's inbox (peer), nullptr at the sink
+  unsigned* succ_flags;   // successor's flags (peer)
+  const unsigned* my_ack; // ACKs written by my successor
+  T* recv_out;
+  T* scanned_out;
+};
+
+__device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ float scan_update(float gl, float r, float x) {
+  return __fadd_rn(__fmul_rn(expf(gl), r), x);
+}
+__device__ __forceinline__ double scan_update(double gl, double r, double x) {
+  return __dadd_rn(__dmul_rn(exp(gl), r), x);
+}
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ bool spin_until_geq(const unsigned* p, unsigned target) {
+  long long t0 = clock64();
+  while ((int)(ld_acquire_sys(p) - target) < 0) {
+    if (clock64() - t0 > (1ll << 34)) return false;  // ~8 s at 2 GHz: treat as deadlock
+  }
+  return true;
+}
+
+// one CTA's share of the chain for one rank
+template <typename T>
+__device__ void rank_body(const Link<T>& L, int h, int dk, int dv, int K, int cta, int nctas, unsigned epoch,
+                          int* err) {
+  const int rows = dk / K;
+  const int blk_el = rows * dv;          // elements of one head inside one pipeline block
+  const int per_cta = (blk_el + nctas - 1) / nctas;
+  const int lo = cta * per_cta, hi = min(blk_el, lo + per_cta);
+  __shared__ int ok;
+  for (int b = 0; b < K; ++b) {
+    const int fidx = b * nctas + cta;
+    if (threadIdx.x == 0) {
+      bool good = true;
+      if (L.inbox) good = spin_until_geq(L.flags + fidx, epoch);
+      if (good && L.succ_inbox) good = spin_until_geq(L.my_ack + fidx, epoch - 1);
+      ok = good;
+      if (!good) {
+        atomicExch(err, 1);
+        printf("zgla all-scan: flag wait timed out (deadlock), block %d\n", b);
+        __trap();
+      }
+    }
+    __syncthreads();
+    if (!ok) return;
+    for (int hh = 0; hh < h; ++hh) {
+      const long long base = (long long)hh * dk * dv + (long long)b * blk_el;
+      for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const long long e = base + i;
+        const int c = b * rows + i / dv;
+        const T r = L.inbox ? ldcg(L.inbox + e) : T(0);
+        // same rounding sequence as the reference update (gate * recv, then + local)
+        const T s = scan_update(L.logdecay[hh * dk + c], r, L.local[e]);
+        if (L.recv_out) L.recv_out[e] = r;
+        L.scanned_out[e] = s;
+        if (L.succ_inbox) L.succ_inbox[e] = s;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      if (L.succ_inbox) st_release_sys(L.succ_flags + fidx, epoch);
+      if (L.ack_to_pred) st_release_sys(L.ack_to_pred + fidx, epoch);
+    }
+  }
+}
+
+// list form: P ranks on one device, recv[p] doubles as rank p's inbox
+template <typename T>
+__global__ void __launch_bounds__(kThreads) local_chain_kernel(int P, int h, int dk, int dv, int K, int dir,
+                                                               const T* local, const T* logdecay, T* recv,
+                                                               T* scanned, unsigned* flags, int* err) {
+  const int pos = blockIdx.x / kCtasPerRank, cta = blockIdx.x % kCtasPerRank;
+  const int rank = dir == ZGLA_FWD ? pos : P - 1 - pos;
+  const long long nel = (long long)h * dk * dv;
+  const int succ = dir == ZGLA_FWD ? rank + 1 : rank - 1;
+  const int fl = K * kCtasPerRank;
+  Link<T> L;
+  L.local = local + rank * nel;
+  L.logdecay = logdecay + (long long)rank * h * dk;
+  L.inbox = pos == 0 ? nullptr : recv + rank * nel;
+  L.flags = flags + (long long)rank * fl;
+  L.ack_to_pred = nullptr;
+  L.succ_inbox = pos == P - 1 ? nullptr : recv + (long long)succ * nel;
+  L.succ_flags = pos == P - 1 ? nullptr : flags + (long long)succ * fl;
+  L.my_ack = nullptr;
+  L.recv_out = pos == 0 ? recv + rank * nel : nullptr;  // source writes its zero recv
+  L.scanned_out = scanned + rank * nel;
+  if (L.succ_inbox) {
+    // no ACK protocol needed: flags are cleared before every list-form call
+    L.my_ack = flags + (long long)P * fl;  // all-zero dummy; epoch-1 == 0 passes
+  }
+  rank_body(L, h, dk, dv, K, cta, kCtasPerRank, 1u, err);
+}
+
+// SPMD form: one rank per process
+__global__ void __launch_bounds__(kThreads) rank_chain_kernel(Link<float> L, int h, int dk, int dv, int K, unsigned epoch,
+                                                              int* err) {
+  rank_body(L, h, dk, dv, K, blockIdx.x, gridDim.x, epoch, err);
+}
+
+__global__ void copy_kernel(long long n, const float* src, float* dst) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = __ldcg(src + i);
+}
+
+// list-form workspace (flags + error word), grown on demand
+struct Scratch {
+  std::mutex mu;
+  unsigned* flags = nullptr;
+  size_t bytes = 0;
+};
+static Scratch g_scratch;
+
+}  // namespace allscan
+}  // namespace zgla
+
+using namespace zgla;
+using namespace zgla::allscan;
+
+extern "C" int zgla_allscan_local(int P, int heads, int key_dim, int value_dim, int dtype, int num_blocks,
+                                  int direction, const void* local_states, const void* log_decays, void* recv,
+                                  void* scanned, void* stream) {
+  if (P < 1 || heads < 1 || key_dim < 1 || value_dim < 1) return ZGLA_ERR_DIMS;
+  if (num_blocks < 1 || key_dim % num_blocks) return ZGLA_ERR_CONFIG;
+  if (direction != ZGLA_FWD && direction != ZGLA_BWD) return ZGLA_ERR_CONFIG;
+  if (dtype != ZGLA_F32 && dtype != ZGLA_F64) return ZGLA_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t fl = (size_t)num_blocks * kCtasPerRank;
+  const size_t need = ((size_t)(P + 1) * fl + 1) * sizeof(unsigned);
+  std::lock_guard<std::mutex> lock(g_scratch.mu);
+  if (g_scratch.bytes < need) {
+    if (g_scratch.flags) cudaFree(g_scratch.flags);
+    g_scratch.flags = nullptr;
+    g_scratch.bytes = 0;
+    if (cudaError_t e = cudaMalloc(&g_scratch.flags, need)) return cuda_fail(e, "zgla_allscan_local");
+    g_scratch.bytes = need;
+  }
+  if (cudaError_t e = cudaMemsetAsync(g_scratch.flags, 0, need, st)) return cuda_fail(e, "zgla_allscan_local");
+  int* err = reinterpret_cast<int*>(g_scratch.flags + (P + 1) * fl);
+  if (dtype == ZGLA_F64)
+    local_chain_kernel<double><<<P * kCtasPerRank, kThreads, 0, st>>>(
+        P, heads, key_dim, value_dim, num_blocks, direction, (const double*)local_states, (const double*)log_decays,
+        (double*)recv, (double*)scanned, g_scratch.flags, err);
+  else
+    local_chain_kernel<float><<<P * kCtasPerRank, kThreads, 0, st>>>(
+        P, heads, key_dim, value_dim, num_blocks, direction, (const float*)local_states, (const float*)log_decays,
+        (float*)recv, (float*)scanned, g_scratch.flags, err);
+  return zgla_check_launch();
+}
+
+// ------------------------------------------------------------------ SPMD comm
+struct zgla_allscan_comm {
+  int rank, world, h, dk, dv, max_blocks;
+  long long nel;
+  size_t region_bytes;
+  unsigned char* region;  // [dir][inbox | flags | ack]
+  unsigned char* next_region;
+  unsigned char* prev_region;
+  bool next_ipc, prev_ipc;
+  unsigned epoch[2];
+  int* err;
+  long long bytes_sent;
+};
+
+static size_t dir_bytes(const zgla_allscan_comm* c) {
+  const size_t fl = (size_t)c->max_blocks * kCtasPerRank * sizeof(unsigned);
+  size_t inbox = (size_t)c->nel * sizeof(float);
+  inbox = (inbox + 255) & ~size_t(255);
+  return inbox + 2 * fl;
+}
+static float* inbox_of(const zgla_allscan_comm* c, unsigned char* region, int dir) {
+  return reinterpret_cast<float*>(region + dir * dir_bytes(c));
+}
+static unsigned* flags_of(const zgla_allscan_comm* c, unsigned char* region, int dir) {
+  size_t inbox = ((size_t)c->nel * sizeof(float) + 255) & ~size_t(255);
+  return reinterpret_cast<unsigned*>(region + dir * dir_bytes(c) + inbox);
+}
+static unsigned* ack_of(const zgla_allscan_comm* c, unsigned char* region, int dir) {
+  return flags_of(c, region, dir) + (size_t)c->max_blocks * kCtasPerRank;
+}
+
+extern "C" int zgla_allscan_create(int rank, int world, int heads, int key_dim, int value_dim, int max_blocks,
+                                   zgla_allscan_comm** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world || heads < 1 || key_dim < 1 || value_dim < 1 ||
+      max_blocks < 1)
+    return ZGLA_ERR_DIMS;
+  auto* c = new zgla_allscan_comm();
+  c->rank = rank;
+  c->world = world;
+  c->h = heads;
+  c->dk = key_dim;
+  c->dv = value_dim;
+  c->max_blocks = max_blocks;
+  c->nel = (long long)heads * key_dim * value_dim;
+  c->region_bytes = 2 * dir_bytes(c);
+  c->epoch[0] = c->epoch[1] = 0;
+  c->bytes_sent = 0;
+  c->next_region = c->prev_region = nullptr;
+  c->next_ipc = c->prev_ipc = false;
+  if (cudaError_t e = cudaMalloc(&c->region, c->region_bytes)) {
+    delete c;
+    return cuda_fail(e, "zgla_allscan_create");
+  }
+  cudaMemset(c->region, 0, c->region_bytes);
+  if (cudaError_t e = cudaMalloc(&c->err, sizeof(int))) {
+    cudaFree(c->region);
+    delete c;
+    return cuda_fail(e, "zgla_allscan_create");
+  }
+  cudaMemset(c->err, 0, sizeof(int));
+  if (cudaError_t e = cudaDeviceSynchronize()) return cuda_fail(e, "zgla_allscan_create");
+  *out = c;
+  return ZGLA_OK;
+}
+
+extern "C" int zgla_allscan_export(zgla_allscan_comm* c, void* ipc_handle_out) {
+  if (!c || !ipc_handle_out) return ZGLA_ERR_DIMS;
+  cudaIpcMemHandle_t h;
+  if (cudaError_t e = cudaIpcGetMemHandle(&h, c->region)) return cuda_fail(e, "zgla_allscan_export");
+  std::memcpy(ipc_handle_out, &h, sizeof(h));
+  return ZGLA_OK;
+}
+
+extern "C" int zgla_allscan_bind(zgla_allscan_comm* c, const void* next_handle, const void* prev_handle) {
+  if (!c) return ZGLA_ERR_DIMS;
+  if (next_handle && c->rank + 1 < c->world) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, next_handle, sizeof(h));
+    void* p = nullptr;
+    if (cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess))
+      return cuda_fail(e, "zgla_allscan_bind(next)");
+    c->next_region = (unsigned char*)p;
+    c->next_ipc = true;
+  }
+  if (prev_handle && c->rank > 0) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, prev_handle, sizeof(h));
+    void* p = nullptr;
+    if (cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess))
+      return cuda_fail(e, "zgla_allscan_bind(prev)");
+    c->prev_region = (unsigned char*)p;
+    c->prev_ipc = true;
+  }
+  return ZGLA_OK;
+}
+
+extern "C" int zgla_allscan_bind_local(zgla_allscan_comm* c, zgla_allscan_comm* next, zgla_allscan_comm* prev) {
+  if (!c) return ZGLA_ERR_DIMS;
+  c->next_region = next ? next->region : nullptr;
+  c->prev_region = prev ? prev->region : nullptr;
+  return ZGLA_OK;
+}
+
+extern "C" int zgla_allscan_run(zgla_allscan_comm* c, int num_blocks, int direction, const float* local_state,
+                                const float* log_decay, float* recv, float* scanned, void* stream) {
+  if (!c || !local_state || !log_decay || !scanned) return ZGLA_ERR_DIMS;
+  if (num_blocks < 1 || num_blocks > c->max_blocks || c->dk % num_blocks) return ZGLA_ERR_CONFIG;
+  if (direction != ZGLA_FWD && direction != ZGLA_BWD) return ZGLA_ERR_CONFIG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d = direction;
+  // chain order: FWD 0 -> P-1, BWD P-1 -> 0
+  const bool is_source = d == ZGLA_FWD ? c->rank == 0 : c->rank == c->world - 1;
+  const bool is_sink = d == ZGLA_FWD ? c->rank == c->world - 1 : c->rank == 0;
+  unsigned char* succ = d == ZGLA_FWD ? c->next_region : c->prev_region;
+  unsigned char* pred = d == ZGLA_FWD ? c->prev_region : c->next_region;
+  if ((!is_sink && !succ) || (!is_source && !pred)) return ZGLA_ERR_STATE;  // not bound
+  const unsigned epoch = ++c->epoch[d];
+  Link<float> L;
+  L.local = local_state;
+  L.logdecay = log_decay;
+  L.inbox = is_source ? nullptr : inbox_of(c, c->region, d);
+  L.flags = flags_of(c, c->region, d);
+  L.ack_to_pred = is_source ? nullptr : ack_of(c, pred, d);
+  L.succ_inbox = is_sink ? nullptr : inbox_of(c, succ, d);
+  L.succ_flags = is_sink ? nullptr : flags_of(c, succ, d);
+  L.my_ack = ack_of(c, c->region, d);
+  L.recv_out = nullptr;
+  L.scanned_out = scanned;
+  if (c->world == 1) L.inbox = nullptr;
+  rank_chain_kernel<<<kCtasPerRank, kThreads, 0, st>>>(L, c->h, c->dk, c->dv, num_blocks, epoch, c->err);
+  if (int rc = zgla_check_launch()) return rc;
+  if (recv) {
+    if (L.inbox)
+      copy_kernel<<<(unsigned)((c->nel + 255) / 256), 256, 0, st>>>(c->nel, L.inbox, recv);
+    else
+      cudaMemsetAsync(recv, 0, c->nel * sizeof(float), st);
+  }
+  if (!is_sink) c->bytes_sent += c->nel * (long long)sizeof(float);
+  return zgla_check_launch();
+}
+
+extern "C" long long zgla_allscan_bytes_sent(const zgla_allscan_comm* c) { return c ? c->bytes_sent : -1; }
+
+extern "C" int zgla_allscan_destroy(zgla_allscan_comm* c) {
+  if (!c) return ZGLA_OK;
+  cudaDeviceSynchronize();
+  if (c->next_ipc && c->next_region) cudaIpcCloseMemHandle(c->next_region);
+  if (c->prev_ipc && c->prev_region) cudaIpcCloseMemHandle(c->prev_region);
+  cudaFree(c->region);
+  cudaFree(c->err);
+  delete c;
+  return ZGLA_OK;
+}

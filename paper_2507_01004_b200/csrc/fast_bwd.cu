@@ -1,0 +1,444 @@
+// Fused tcgen05 ZeCO GLA backward (reference glasp/gla.py:359-444, paper Alg. 3),
+// bf16 q/k/v/dO/dq/dk/dv, fp32 g/dg/states, D = 128, 64-token tiles.
+//
+// One CTA per (head, segment) walks its tiles RIGHT TO LEFT carrying the fp32
+// state cotangent D (registers of 8 warps), seeded with the lifted segment-end
+// cotangent  D_end = Dend_loc + e^{G_L - G_end} ds_next  (fused bwd correction).
+// The forward chunk-start states come from the forward kernel (saved as
+// S'_n = e^{r_n} S_n in bf16), so no forward recomputation walk is needed.
+// Per tile (Qh = Q e^{logb-r}, Kh = K e^{r-logb}, D' = e^{gam-r} D_{n+1}):
+//   A    = Qh Kh^T      dP = dO V^T                 (M=64, N=64)   masked in registers
+//   QDO' = Qh^T dO                                   (M=128,N=128)  D_n = e^gam D + e^r QDO'
+//   dq^T = Kh^T dPm^T + S' dO^T                      (M=128,N=64)   dq = E (.) dq_raw
+//   dk^T = Qh^T dPm   + D' V^T                       (M=128,N=64)   dk = dk_raw / E
+//   dv^T = dO^T Am    + D'^T Kh^T                    (M=128,N=64)
+// All gradient accumulators are TRANSPOSED (channels on TMEM lanes), so the
+// epilogue thread of channel c owns a token column and computes
+//   da_t = Qh (.) dq_raw - Kh (.) dk_raw  (= q.dq - k.dk)
+//   dg_t = sum_{t' >= t in tile} da_t' + rho_{n+1},   rho_n = rho_{n+1} + sum_tile da
+// sequentially, where rho at the segment end is rowsum(S_end (.) D_end): the
+// suffix sum of da beyond a boundary equals that boundary rowsum, so dg needs
+// no cross-segment pass (it includes the reference's tail term,
+// glasp/gla.py:440-443, at the shard end).
+#include "fast_common.cuh"
+
+namespace zgla {
+namespace fast {
+
+constexpr int BO_NS = 2;
+constexpr int BO_STAGE = 4 * TILE_BF16;  // q, k, v, dO
+constexpr int BO_THREADS = 448;          // 8 state warps, 4 prep warps, TMA warp, MMA warp
+constexpr int BO_OFF_SP = BO_NS * BO_STAGE;
+constexpr int BO_OFF_DP = BO_OFF_SP + STATE_BF16;
+constexpr int BO_OFF_AM = BO_OFF_DP + STATE_BF16;
+constexpr int BO_OFF_DPM = BO_OFF_AM + T * T * 2;
+constexpr int BO_OFF_VEC = BO_OFF_DPM + T * T * 2;
+constexpr int BO_OFF_X = BO_OFF_VEC + BO_NS * 2 * D * 4;
+constexpr int BO_OFF_BAR = BO_OFF_X + 4096;
+constexpr size_t BO_SMEM = 1024 + BO_OFF_BAR + 256;
+constexpr uint32_t BC_DQ = 0, BC_DK = 64, BC_DV = 128, BC_QDO = 192, BC_A = 320, BC_DPC = 384;
+
+__global__ void __launch_bounds__(BO_THREADS, 1)
+    bwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+                   const __grid_constant__ CUtensorMap tm_sp, const float* __restrict__ g, long long L, int nseg,
+                   int ntiles, const float* __restrict__ Sin, const float* __restrict__ cumG,
+                   const float* __restrict__ dS, const float* __restrict__ gamseg, const float* __restrict__ s_prev,
+                   const float* __restrict__ Dend, const float* __restrict__ cumGr,
+                   const float* __restrict__ ds_next, __nv_bfloat16* __restrict__ dq, __nv_bfloat16* __restrict__ dk,
+                   __nv_bfloat16* __restrict__ dv, float* __restrict__ dg) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sp_buf = smem + BO_OFF_SP;
+  uint8_t* dp_buf = smem + BO_OFF_DP;
+  uint8_t* am_buf = smem + BO_OFF_AM;
+  uint8_t* dpm_buf = smem + BO_OFF_DPM;
+  float* vgam = reinterpret_cast<float*>(smem + BO_OFF_VEC);
+  float* vr = vgam + BO_NS * D;
+  float2* xa = reinterpret_cast<float2*>(smem + BO_OFF_X);  // prep exchange (64 + 64 float2)
+  float2* xb = xa + 64;
+  float* xrho = reinterpret_cast<float*>(smem + BO_OFF_X + 1024);  // [2][D] row-sum partials
+  float* xtot = xrho + 2 * D;                                      // [D] logb of row 31 (epilogue)
+  float* xcarry = xtot + D;                                        // [2][D] per-half sums of da
+  float* xr = xcarry + 2 * D;                                      // [D] rho at the current tile end
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + BO_OFF_BAR);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + BO_NS;
+  uint64_t* prep = bars + 2 * BO_NS;
+  uint64_t* sc_full = bars + 3 * BO_NS;
+  uint64_t* sc_done = sc_full + 1;
+  uint64_t* qdo_full = sc_full + 2;
+  uint64_t* qdo_empty = sc_full + 3;
+  uint64_t* dp_ready = sc_full + 4;
+  uint64_t* grads_full = sc_full + 5;
+  uint64_t* grads_empty = sc_full + 6;
+  uint64_t* sp_full = sc_full + 7;
+  uint64_t* sp_empty = sc_full + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sc_full + 9);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int hh = blockIdx.x / nseg, s = blockIdx.x % nseg;
+  int t0, t1;
+  seg_range(s, nseg, ntiles, t0, t1);
+  const int nt = t1 - t0;
+  const int row0 = (int)(hh * L);
+
+  if (tid == 0) {
+    for (int i = 0; i < BO_NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 256);
+      mbar_init(&prep[i], 128);
+    }
+    mbar_init(sc_full, 1);
+    mbar_init(sc_done, 256);
+    mbar_init(qdo_full, 1);
+    mbar_init(qdo_empty, 256);
+    mbar_init(dp_ready, 256);
+    mbar_init(grads_full, 1);
+    mbar_init(grads_empty, 256);
+    mbar_init(sp_full, 1);
+    mbar_init(sp_empty, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 12) {
+    // ---------------- TMA producer (tiles right to left)
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      tma_prefetch_desc(&tm_do);
+      tma_prefetch_desc(&tm_sp);
+      for (int m = 0; m < nt; ++m) {
+        const int st = m % BO_NS, ph = (m / BO_NS) & 1;
+        const int n = t1 - 1 - m;
+        uint8_t* sb = smem + st * BO_STAGE;
+        mbar_wait(&empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&full[st], BO_STAGE);
+        const int r = row0 + n * T;
+        tma_load_2d(sb, &tm_q, &full[st], 0, r);
+        tma_load_2d(sb + PANEL, &tm_q, &full[st], 64, r);
+        tma_load_2d(sb + TILE_BF16, &tm_k, &full[st], 0, r);
+        tma_load_2d(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r);
+        tma_load_2d(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r);
+        tma_load_2d(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r);
+        tma_load_2d(sb + 3 * TILE_BF16, &tm_do, &full[st], 0, r);
+        tma_load_2d(sb + 3 * TILE_BF16 + PANEL, &tm_do, &full[st], 64, r);
+        mbar_wait(sp_empty, (m & 1) ^ 1);
+        mbar_arrive_expect_tx(sp_full, STATE_BF16);
+        const int rs = (hh * ntiles + n) * D;
+        tma_load_2d(sp_buf, &tm_sp, sp_full, 0, rs);
+        tma_load_2d(sp_buf + SPANEL, &tm_sp, sp_full, 64, rs);
+      }
+    }
+  } else if (warp == 13) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id_sc = idesc_bf16(64, 64, false, false);
+      constexpr uint32_t id_qdo = idesc_bf16(128, 128, true, true);
+      constexpr uint32_t id_mk = idesc_bf16(128, 64, true, false);
+      constexpr uint32_t id_kk = idesc_bf16(128, 64, false, false);
+      constexpr uint32_t id_mm = idesc_bf16(128, 64, true, true);
+      const uint32_t spa = smem_u32(sp_buf), dpa = smem_u32(dp_buf);
+      const uint32_t ama = smem_u32(am_buf), dpma = smem_u32(dpm_buf);
+      for (int m = 0; m < nt; ++m) {
+        const int st = m % BO_NS, ph = (m / BO_NS) & 1;
+        const uint32_t qa = smem_u32(smem + st * BO_STAGE);
+        const uint32_t ka = qa + TILE_BF16, va = qa + 2 * TILE_BF16, da = qa + 3 * TILE_BF16;
+        mbar_wait(&prep[st], ph);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {  // scores and dP, K = 128 channels
+          const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
+          mma_bf16_ss(tbase + BC_A, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_sc, kk > 0);
+          mma_bf16_ss(tbase + BC_DPC, sdesc(da + off, 16, 1024), sdesc(va + off, 16, 1024), id_sc, kk > 0);
+        }
+        mma_commit(sc_full);
+        mbar_wait(qdo_empty, (m & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)
+          mma_bf16_ss(tbase + BC_QDO, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(da + kk * 2048, PANEL, 1024),
+                      id_qdo, kk > 0);
+        mma_commit(qdo_full);
+        mbar_wait(sc_done, m & 1);
+        mbar_wait(grads_empty, (m & 1) ^ 1);
+        mbar_wait(sp_full, m & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)  // dq^T = Kh^T dPm^T
+          mma_bf16_ss(tbase + BC_DQ, sdesc(ka + kk * 2048, PANEL, 1024), sdesc(dpma + kk * 32, 16, 1024), id_mk,
+                      kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)  // dq^T += S' dO^T
+          mma_bf16_ss(tbase + BC_DQ, sdesc(spa + (kk >> 2) * SPANEL + (kk & 3) * 32, 16, 1024),
+                      sdesc(da + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024), id_kk, 1);
+        mma_commit(sp_empty);
+        mbar_wait(dp_ready, m & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk) {  // dk^T = Qh^T dPm ; dv^T = dO^T Am
+          mma_bf16_ss(tbase + BC_DK, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(dpma + kk * 2048, PANEL, 1024), id_mm,
+                      kk > 0);
+          mma_bf16_ss(tbase + BC_DV, sdesc(da + kk * 2048, PANEL, 1024), sdesc(ama + kk * 2048, PANEL, 1024), id_mm,
+                      kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {  // dk^T += D' V^T ; dv^T += D'^T Kh^T
+          const uint32_t boff = (kk >> 2) * PANEL + (kk & 3) * 32;
+          mma_bf16_ss(tbase + BC_DK, sdesc(dpa + (kk >> 2) * SPANEL + (kk & 3) * 32, 16, 1024),
+                      sdesc(va + boff, 16, 1024), id_kk, 1);
+          mma_bf16_ss(tbase + BC_DV, sdesc(dpa + kk * 2048, SPANEL, 1024), sdesc(ka + boff, 16, 1024), id_mk, 1);
+        }
+        mma_commit(grads_full);
+      }
+    }
+  } else if (warp >= 8) {
+    // ---------------- prep: logb, r, Qh / Kh in place (g read straight from global)
+    const int t = tid - 256;
+    const int cp = t & 63, rh = t >> 6;
+    for (int m = 0; m < nt; ++m) {
+      const int st = m % BO_NS, ph = (m / BO_NS) & 1;
+      const int n = t1 - 1 - m;
+      uint8_t* sb = smem + st * BO_STAGE;
+      float2 lb[32];  // gates, then their in-chunk prefix (in place)
+      const float* gp = g + ((long long)row0 + n * T + 32 * rh) * D + 2 * cp;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) lb[r] = __ldg(reinterpret_cast<const float2*>(gp + r * D));
+      float run0 = 0.f, run1 = 0.f;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        run0 += lb[r].x;
+        run1 += lb[r].y;
+        lb[r] = make_float2(run0, run1);
+      }
+      mbar_wait(&full[st], ph);
+      if (rh == 0) xa[cp] = make_float2(run0, run1);
+      named_bar(1, 128);
+      const float2 half = xa[cp];
+      float off0 = 0.f, off1 = 0.f;
+      if (rh == 1) {
+        off0 = half.x;
+        off1 = half.y;
+        xb[cp] = make_float2(half.x + run0, half.y + run1);
+      }
+      named_bar(1, 128);
+      if (rh == 0) {
+        const float2 gam = xb[cp];
+        vgam[st * D + 2 * cp] = gam.x;
+        vgam[st * D + 2 * cp + 1] = gam.y;
+        vr[st * D + 2 * cp] = half.x;
+        vr[st * D + 2 * cp + 1] = half.y;
+      }
+      constexpr float LOG2E = 1.4426950408889634f;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const float d0 = (lb[r].x + off0 - half.x) * LOG2E, d1 = (lb[r].y + off1 - half.y) * LOG2E;
+        const uint32_t o = pair_off(32 * rh + r, cp, PANEL);
+        uint32_t* pq = reinterpret_cast<uint32_t*>(sb + o);
+        uint32_t* pk = reinterpret_cast<uint32_t*>(sb + TILE_BF16 + o);
+        const float2 qv = unpack_bf16(*pq), kv = unpack_bf16(*pk);
+        *pq = pack_bf16(qv.x * fast_exp2(d0), qv.y * fast_exp2(d1));
+        *pk = pack_bf16(kv.x * fast_exp2(-d0), kv.y * fast_exp2(-d1));
+      }
+      fence_proxy_async();
+      mbar_arrive(&prep[st]);
+    }
+  } else {
+    // ---------------- state / epilogue warps
+    const int qd = warp & 3, ch = warp >> 2;
+    const int c = 32 * qd + lane;
+    float Dst[64];
+    {
+      const long long sidx = ((long long)(hh * nseg + s) * D + c) * D + 64 * ch;
+      const float cgr = ds_next ? expf(cumGr[(hh * nseg + s) * D + c]) : 0.f;
+      const float cg = s_prev ? expf(cumG[(hh * nseg + s) * D + c]) : 0.f;
+      const float eg = expf(gamseg[(hh * nseg + s) * D + c]);
+      const float* pn = ds_next ? ds_next + ((long long)hh * D + c) * D + 64 * ch : nullptr;
+      const float* pp = s_prev ? s_prev + ((long long)hh * D + c) * D + 64 * ch : nullptr;
+      float rho = 0.f;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        float dd = Dend[sidx + j];
+        if (pn) dd += cgr * pn[j];
+        Dst[j] = dd;
+        float si = Sin[sidx + j];
+        if (pp) si += cg * pp[j];
+        const float se = eg * si + dS[sidx + j];  // fp32 forward state at the segment end
+        rho += se * dd;
+      }
+      xrho[ch * D + c] = rho;
+    }
+    named_bar(2, 256);
+    if (ch == 0) xr[c] = xrho[c] + xrho[D + c];
+    for (int m = 0; m < nt; ++m) {
+      const int st = m % BO_NS, ph = (m / BO_NS) & 1;
+      const int n = t1 - 1 - m;
+      // (a) masked scores / dP -> bf16 operands
+      mbar_wait(sc_full, m & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        float a[32];
+        tmem_ld32(taddr(tbase, 32 * qd, (which ? BC_DPC : BC_A) + 32 * ch), a);
+        uint8_t* dstbuf = which ? dpm_buf : am_buf;
+        if (lane < 16) {
+          const int i = 16 * qd + lane;
+#pragma unroll
+          for (int mm = 0; mm < 4; ++mm) {
+            const int j0 = 32 * ch + 8 * mm;
+            float x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = (j0 + u <= i) ? a[8 * mm + u] : 0.f;
+            uint4 w;
+            w.x = pack_bf16(x[0], x[1]);
+            w.y = pack_bf16(x[2], x[3]);
+            w.z = pack_bf16(x[4], x[5]);
+            w.w = pack_bf16(x[6], x[7]);
+            *reinterpret_cast<uint4*>(dstbuf + sw128(i, 4 * ch + mm)) = w;
+          }
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(sc_done);
+      // (b) D' = e^{gam - r} D_{n+1} -> bf16 [c][v]
+      mbar_wait(&prep[st], ph);
+      const float gam_c = vgam[st * D + c], r_c = vr[st * D + c];
+      {
+        const float sc = fast_exp(gam_c - r_c);
+        uint8_t* dst = dp_buf + ch * SPANEL;
+#pragma unroll
+        for (int mm = 0; mm < 8; ++mm) {
+          uint4 w;
+          w.x = pack_bf16(Dst[8 * mm] * sc, Dst[8 * mm + 1] * sc);
+          w.y = pack_bf16(Dst[8 * mm + 2] * sc, Dst[8 * mm + 3] * sc);
+          w.z = pack_bf16(Dst[8 * mm + 4] * sc, Dst[8 * mm + 5] * sc);
+          w.w = pack_bf16(Dst[8 * mm + 6] * sc, Dst[8 * mm + 7] * sc);
+          *reinterpret_cast<uint4*>(dst + sw128(c, mm)) = w;
+        }
+      }
+      fence_proxy_async();
+      mbar_arrive(dp_ready);
+      // (c) D_n = e^{gam} D_{n+1} + e^{r} QDO'
+      mbar_wait(qdo_full, m & 1);
+      tc_fence_after();
+      {
+        const float eg = fast_exp(gam_c), er = fast_exp(r_c);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          float x[32];
+          tmem_ld32(taddr(tbase, 32 * qd, BC_QDO + 64 * ch + 32 * hf), x);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) Dst[32 * hf + j] = eg * Dst[32 * hf + j] + er * x[j];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(qdo_empty);
+      // (d) epilogue: thread owns channel c, tokens [32*ch, 32*ch+32) of the tile.
+      //     pass 1: T = sum of da over my tokens (da = Qh dq_raw - Kh dk_raw needs no exponentials)
+      //     pass 2 (token order): logb, E, dq/dk/dv stores, dg_i = base - prefix_{<i}(da)
+      mbar_wait(grads_full, m & 1);
+      tc_fence_after();
+      const uint8_t* sb = smem + st * BO_STAGE;
+      const uint32_t cbase = (c >> 6) * PANEL + (c & 7) * 2;
+      const uint32_t cchunk = (c & 63) >> 3;
+      float tsum = 0.f;
+#pragma unroll
+      for (int q8 = 0; q8 < 4; ++q8) {
+        float gq[8], gk[8];
+        tmem_ld8(taddr(tbase, 32 * qd, BC_DQ + 32 * ch + 8 * q8), gq);
+        tmem_ld8(taddr(tbase, 32 * qd, BC_DK + 32 * ch + 8 * q8), gk);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t o = cbase + sw128(32 * ch + 8 * q8 + u, cchunk);
+          const float qh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + o));
+          const float kh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + TILE_BF16 + o));
+          tsum += qh * gq[u] - kh * gk[u];
+        }
+      }
+      // logb of my first token needs the sum of the gates before it (upper half: rows 0..31 of the tile)
+      const float* gp = g + ((long long)row0 + n * T + 32 * ch) * D + c;
+      float gsum = 0.f;
+      if (ch == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) gsum += __ldg(gp + (long long)i * D);
+        xtot[c] = gsum;
+      }
+      xcarry[ch * D + c] = tsum;
+      named_bar(2, 256);
+      const float rho_end = xr[c];
+      const float t_upper = xcarry[D + c], t_lower = xcarry[c];
+      // dg_i = rho_{n+1} + sum_{i' >= i} da  ->  base = rho + (da of my half and every later half)
+      float base = rho_end + (ch == 0 ? t_lower + t_upper : t_upper);
+      float lb = ch ? xtot[c] : 0.f;
+      const long long tok0 = (long long)row0 + n * T + 32 * ch;
+      constexpr float LOG2E = 1.4426950408889634f;
+#pragma unroll
+      for (int q8 = 0; q8 < 4; ++q8) {
+        float gq[8], gk[8], gv8[8], gg[8];
+        tmem_ld8(taddr(tbase, 32 * qd, BC_DQ + 32 * ch + 8 * q8), gq);
+        tmem_ld8(taddr(tbase, 32 * qd, BC_DK + 32 * ch + 8 * q8), gk);
+        tmem_ld8(taddr(tbase, 32 * qd, BC_DV + 32 * ch + 8 * q8), gv8);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) gg[u] = __ldg(gp + (long long)(8 * q8 + u) * D);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = 8 * q8 + u;
+          lb += gg[u];
+          const float dlt = (lb - r_c) * LOG2E;
+          const uint32_t o = cbase + sw128(32 * ch + i, cchunk);
+          const float qh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + o));
+          const float kh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + TILE_BF16 + o));
+          dq[(tok0 + i) * D + c] = __float2bfloat16_rn(gq[u] * fast_exp2(dlt));
+          dk[(tok0 + i) * D + c] = __float2bfloat16_rn(gk[u] * fast_exp2(-dlt));
+          dv[(tok0 + i) * D + c] = __float2bfloat16_rn(gv8[u]);
+          dg[(tok0 + i) * D + c] = base;
+          base -= qh * gq[u] - kh * gk[u];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(grads_empty);
+      mbar_arrive(&empty[st]);  // stage reads (Qh, Kh) done
+      named_bar(2, 256);        // everyone has read xr / xcarry / xtot of this tile
+      if (ch == 0) xr[c] = rho_end + t_lower + t_upper;  // rho at the start of this tile
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+}  // namespace fast
+
+using namespace fast;
+
+int fast_bwd_output(const zgla_shape* s, int num_sms, const void* q, const void* k, const void* v, const void* g,
+                    const void* d_out, void* ws, const void* s_prev, const void* ds_next, void* dq, void* dk,
+                    void* dv, void* dg, cudaStream_t st) {
+  const Plan pl = make_plan(s, num_sms);
+  Ws w = carve(pl, ws);
+  CUtensorMap mq, mk, mv, mdo, msp;
+  const unsigned long long rows = (unsigned long long)pl.h * pl.L;
+  if (int rc = make_map(&mq, q, true, rows, D, 64, T, true)) return rc;
+  if (int rc = make_map(&mk, k, true, rows, D, 64, T, true)) return rc;
+  if (int rc = make_map(&mv, v, true, rows, D, 64, T, true)) return rc;
+  if (int rc = make_map(&mdo, d_out, true, rows, D, 64, T, true)) return rc;
+  if (int rc = make_map(&msp, w.Sp, true, (unsigned long long)pl.h * pl.ntiles * D, D, 64, D, true)) return rc;
+  cudaFuncSetAttribute(bwd_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BO_SMEM);
+  bwd_out_kernel<<<pl.h * pl.nseg, BO_THREADS, BO_SMEM, st>>>(
+      mq, mk, mv, mdo, msp, (const float*)g, pl.L, pl.nseg, pl.ntiles, w.Sin, w.cumG, w.dS, w.gam,
+      (const float*)s_prev, w.Dend, w.cumGr, (const float*)ds_next, (__nv_bfloat16*)dq, (__nv_bfloat16*)dk,
+      (__nv_bfloat16*)dv, (float*)dg);
+  return zgla_check_launch();
+}
+
+}  // namespace zgla

@@ -1,0 +1,138 @@
+// Shared pieces of the fused tcgen05 ZeCO kernels (bf16 storage, fp32 state).
+//
+// Geometry: head dim D = dk = dv = 128, tile T = 64 tokens.  Each head's shard
+// of L tokens (NT = L/64 tiles) is cut into `nseg` contiguous SEGMENTS, one CTA
+// each, so the grid is heads x nseg ~ one wave of 148 SMs.  The ZeCO identity
+// (Appendix A) is applied *inside* the GPU as well: every
+// segment first computes its local state contribution from zero, a small
+// elementwise scan over segments gives each segment its incoming state, and
+// the output kernel starts from that state.  Across GPUs the same identity is
+// applied once more by All-Scan.
+#pragma once
+#include <cudaTypedefs.h>
+
+#include "tc.cuh"
+#include "zgla_internal.h"
+
+namespace zgla {
+namespace fast {
+
+constexpr int D = 128;                 // head dim (dk = dv)
+constexpr int T = 64;                  // tokens per tile
+constexpr int PANEL = T * 128;         // one 64-column SW128 panel of a [64 x D] bf16 tile (8 KiB)
+constexpr int TILE_BF16 = T * D * 2;   // 16 KiB
+constexpr int TILE_F32 = T * D * 4;    // 32 KiB
+constexpr int SPANEL = D * 128;        // one 64-column panel of a [D x D] bf16 state (16 KiB)
+constexpr int STATE_BF16 = D * D * 2;  // 32 KiB
+
+struct Plan {
+  int h, nseg, ntiles;
+  long long L;
+};
+
+__host__ __device__ inline void seg_range(int s, int nseg, int ntiles, int& t0, int& t1) {
+  t0 = (int)((long long)s * ntiles / nseg);
+  t1 = (int)((long long)(s + 1) * ntiles / nseg);
+}
+
+// workspace carve-up (fp32 unless noted), per shard
+struct Ws {
+  float* dS;      // [h][nseg][D][D]  fwd: segment-local final state from zero
+  float* gam;     // [h][nseg][D]     segment total log decay
+  float* Sin;     // [h][nseg][D][D]  fwd: rank-local state at segment start (exclusive scan)
+  float* cumG;    // [h][nseg][D]     sum of gam over earlier segments
+  float* dD;      // [h][nseg][D][D]  bwd: state cotangent at segment start from the segment's tokens
+  float* Dend;    // [h][nseg][D][D]  bwd: rank-local cotangent at segment end (later segments)
+  float* cumGr;   // [h][nseg][D]     sum of gam over later segments
+  __nv_bfloat16* Sp;  // [h][NT][D][D] bf16: scaled chunk-start states e^{r} S for the backward
+};
+
+inline long long ws_bytes(const Plan& p) {
+  const long long st = (long long)p.h * p.nseg * D * D * 4;
+  const long long vec = (long long)p.h * p.nseg * D * 4;
+  const long long sp = (long long)p.h * p.ntiles * STATE_BF16;
+  return 4 * st + 3 * vec + sp + 4096;
+}
+
+inline Ws carve(const Plan& p, void* base) {
+  const long long st = (long long)p.h * p.nseg * D * D;
+  const long long vec = (long long)p.h * p.nseg * D;
+  float* f = reinterpret_cast<float*>(base);
+  Ws w;
+  w.dS = f;
+  w.Sin = w.dS + st;
+  w.dD = w.Sin + st;
+  w.Dend = w.dD + st;
+  w.gam = w.Dend + st;
+  w.cumG = w.gam + vec;
+  w.cumGr = w.cumG + vec;
+  uintptr_t sp = reinterpret_cast<uintptr_t>(w.cumGr + vec);
+  sp = (sp + 1023) & ~uintptr_t(1023);
+  w.Sp = reinterpret_cast<__nv_bfloat16*>(sp);
+  return w;
+}
+
+inline Plan make_plan(const zgla_shape* s, int num_sms) {
+  Plan p;
+  p.h = s->heads;
+  p.L = s->seq_len;
+  p.ntiles = (int)(s->seq_len / T);
+  int nseg = num_sms / (s->heads > 0 ? s->heads : 1);
+  if (nseg < 1) nseg = 1;
+  if (nseg > p.ntiles) nseg = p.ntiles;
+  p.nseg = nseg;
+  return p;
+}
+
+// ---- host: TMA descriptors via the driver entry point (no libcuda link dependency)
+inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 2-D map over a row-major [rows][cols] tensor
+inline int make_map(CUtensorMap* m, const void* base, bool bf16, unsigned long long rows, unsigned cols,
+                    unsigned box_cols, unsigned box_rows, bool swizzle128) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return ZGLA_ERR_CUDA;
+  }
+  const unsigned eb = bf16 ? 2 : 4;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * eb};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[128];
+    std::snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    set_error(buf);
+    return ZGLA_ERR_CUDA;
+  }
+  return ZGLA_OK;
+}
+
+// ---- device helpers
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// address of the bf16 pair (row, 2*cp .. 2*cp+1) inside a [rows x 128] SW128 tile (2 panels of
+// `panel_bytes` each)
+__device__ __forceinline__ uint32_t pair_off(int row, int cp, int panel_bytes) {
+  return (cp >> 5) * panel_bytes + sw128(row, (cp & 31) >> 2) + (cp & 3) * 4;
+}
+
+}  // namespace fast
+}  // namespace zgla

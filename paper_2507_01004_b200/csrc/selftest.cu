@@ -1,0 +1,95 @@
+// Diagnostic entry point: one tcgen05 MMA tile through the same descriptor /
+// SW128 layout code the GLA kernels use, so a layout or encoding mistake shows
+// up as a wrong 128x128 product instead of a wrong attention output.
+#include "tc.cuh"
+#include "zgla_internal.h"
+
+namespace zgla {
+
+// A operand is M x K, B operand is K x N (math view).  Storage:
+//   A K-major : a_src[M][K]      A MN-major : a_src[K][M]
+//   B K-major : b_src[N][K]      B MN-major : b_src[K][N]
+__global__ void __launch_bounds__(128) selftest_mma_kernel(const __nv_bfloat16* __restrict__ a_src,
+                                                           const __nv_bfloat16* __restrict__ b_src,
+                                                           float* __restrict__ d_out, int M, int N, int K,
+                                                           int a_mn, int b_mn, int lane_off) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x;
+
+  // storage shapes
+  const int a_rows = a_mn ? K : M, a_cols = a_mn ? M : K;
+  const int b_rows = b_mn ? K : N, b_cols = b_mn ? N : K;
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + a_rows * a_cols * 2;  // multiples of 1024 for our shapes
+  auto fill = [&](const __nv_bfloat16* src, int rows, int cols, uint8_t* dst) {
+    const int chunks_per_row = cols / 8;
+    for (int i = tid; i < rows * chunks_per_row; i += blockDim.x) {
+      int r = i / chunks_per_row, c = i % chunks_per_row;
+      int panel = c / 8, cc = c % 8;
+      uint4 val = *reinterpret_cast<const uint4*>(src + r * cols + c * 8);
+      *reinterpret_cast<uint4*>(dst + panel * rows * 128 + sw128(r, cc)) = val;
+    }
+  };
+  fill(a_src, a_rows, a_cols, sa);
+  fill(b_src, b_rows, b_cols, sb);
+  fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core (async proxy)
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (tid < 32) {
+    tmem_alloc(&tmem_base_sh, 256);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base_sh;
+  const uint32_t d_tmem = tbase + (static_cast<uint32_t>(lane_off) << 16);
+
+  if (tid == 0) {
+    const uint32_t idesc = idesc_bf16(M, N, a_mn, b_mn);
+    for (int kk = 0; kk < K / 16; ++kk) {
+      uint64_t ad, bd;
+      if (a_mn) ad = sdesc(smem_u32(sa) + kk * 16 * 128, a_rows * 128, 1024);
+      else ad = sdesc(smem_u32(sa) + (kk / 4) * a_rows * 128 + (kk % 4) * 32, 16, 1024);
+      if (b_mn) bd = sdesc(smem_u32(sb) + kk * 16 * 128, b_rows * 128, 1024);
+      else bd = sdesc(smem_u32(sb) + (kk / 4) * b_rows * 128 + (kk % 4) * 32, 16, 1024);
+      mma_bf16_ss(d_tmem, ad, bd, idesc, kk > 0);
+    }
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  const int warp = tid / 32, lane = tid % 32;
+  // row m of D lives in TMEM lane m (M=128) or lane (m%16)+32*(m/16) (+lane_off) (M=64)
+  int row;
+  if (M == 128) row = warp * 32 + lane;
+  else row = (lane >= lane_off && lane < lane_off + 16) ? warp * 16 + (lane - lane_off) : -1;
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    float v[32];
+    tmem_ld32(taddr(tbase, warp * 32, c0), v);
+    if (row >= 0)
+      for (int j = 0; j < 32; ++j) d_out[row * N + c0 + j] = v[j];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tmem_dealloc(tbase, 256);
+}
+
+}  // namespace zgla
+
+extern "C" int zgla_selftest_mma(const void* a, const void* b, float* d, int M, int N, int K, int a_mn, int b_mn,
+                                 int lane_off, void* stream) {
+  using namespace zgla;
+  if (!((M == 64 || M == 128) && N % 16 == 0 && N <= 256 && K % 64 == 0 && (M == 64 || lane_off == 0)))
+    return ZGLA_ERR_DIMS;
+  size_t smem = 1024 + (size_t)M * K * 2 + (size_t)N * K * 2;
+  cudaFuncSetAttribute(selftest_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  selftest_mma_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)a, (const __nv_bfloat16*)b, d, M, N, K, a_mn, b_mn, lane_off);
+  return zgla_check_launch();
+}
