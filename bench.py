@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark: ZeCO GLA layer forward + backward (BASELINE.json config 2 per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload per rank: one GLA layer, H=16 heads, d_k=d_v=128, 16,384 tokens,
+chunk 64, bf16 q/k/v/dO, fp32 log-gates ~ U(log .9, log .999) (synthetic,
+seeded per rank).  A step = fwd (local scan, All-Scan FWD, outputs with fused
+correction) + bwd (local reverse scan, All-Scan BWD, gradients with fused
+correction).  N>1 is weak scaling (16K tokens per GPU), launched by torchrun.
+
+Prints ONE JSON line on rank 0 (see README "bench contract").
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s/GPU, ZeCO GLA layer fwd+bwd, 1/2/4/8 B200 weak scaling; All-Scan µs"
+UNIT = "tokens/s"
+PEAK_FALLBACK_HBM = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--heads", type=int, default=16)
+    p.add_argument("--seq", type=int, default=16384, help="tokens per GPU")
+    p.add_argument("--dim", type=int, default=128)
+    p.add_argument("--chunk", type=int, default=64)
+    p.add_argument("--blocks", type=int, default=4, help="All-Scan pipeline blocks K")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=5)
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    except Exception:
+        return PEAK_FALLBACK_HBM, 1400.0, "fallback"
+
+
+def bytes_per_token_head(dk, dv):
+    """Algorithmic (compulsory) HBM bytes: bf16 q,k,v,o,dO,dq,dk,dv; fp32 g, dg."""
+    fwd = 8 * dk + 4 * dv
+    bwd = 16 * dk + 6 * dv
+    return fwd, bwd
+
+
+def flops_per_token_head(C, dk, dv):
+    fwd = 2 * C * (dk + dv) + 4 * dk * dv
+    bwd = 2 * C * (3 * dk + 2 * dv) + 12 * dk * dv
+    return fwd, bwd
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons while the timed region runs."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz, self.ok = [], set(), None, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _names(self, mask):
+        nv = self.nv
+        table = {
+            "gpu_idle": getattr(nv, "nvmlClocksEventReasonGpuIdle", 0x1),
+            "applications_clocks_setting": getattr(nv, "nvmlClocksEventReasonApplicationsClocksSetting", 0x2),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sync_boost": getattr(nv, "nvmlClocksEventReasonSyncBoost", 0x10),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        return {k for k, bit in table.items() if mask & bit}
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    self.nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                self.reasons |= self._names(fn(self.h))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+def load_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu summary (profiles/)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("bwd_out_kernel", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU legs (oracle port)
+
+def _cpu_heads(args):
+    """worker: f64 oracle ZeCO fwd+bwd on a subset of heads (single-threaded numpy)."""
+    heads, L, D, C, seed = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import gla_oracle as orc
+    rng = np.random.default_rng(seed)
+    q, k, v = (rng.uniform(-1, 1, (heads, L, D)) for _ in range(3))
+    g = rng.uniform(orc.DECAY_LOW, orc.DECAY_HIGH, (heads, L, D))
+    do = rng.uniform(-1, 1, (heads, L, D))
+    t0 = time.perf_counter()
+    o, saved, _ = orc.zeco_forward(q, k, v, g, 1, C)
+    orc.zeco_backward(q, k, v, g, do, 1, C, saved)
+    return time.perf_counter() - t0
+
+
+def cpu_sample(H, L_sample, D, C, workers, seed=0):
+    """Time the oracle on all H heads of an L_sample-token shard, heads spread over `workers` processes."""
+    import multiprocessing as mp
+    per = [H // workers + (1 if i < H % workers else 0) for i in range(workers)]
+    jobs = [(n, L_sample, D, C, seed + i) for i, n in enumerate(per) if n > 0]
+    t0 = time.perf_counter()
+    if len(jobs) == 1:
+        _cpu_heads(jobs[0])
+    else:
+        ctx = mp.get_context("spawn")
+        with ctx.Pool(len(jobs)) as pool:
+            pool.map(_cpu_heads, jobs)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port, f64 NumPy) on this box's cores."""
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    workers = max(1, min(cores, args.heads))
+    L_sample = 512
+    for _ in range(max(args.warmup, 0)):
+        cpu_sample(args.heads, L_sample, args.dim, args.chunk, workers)
+    times = [cpu_sample(args.heads, L_sample, args.dim, args.chunk, workers) for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    rate = L_sample / t  # tokens/s of one rank's shard (all heads)
+    sample = f"all {args.heads} heads x {L_sample} tokens, d={args.dim}, C={args.chunk}, f64, per step"
+    line = {
+        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": "GLA layer fwd+bwd (cfg2: H=16, d=128, 16K tok/GPU), CPU sample", "heads": args.heads,
+                   "head_dim": args.dim, "chunk": args.chunk, "tokens_per_gpu": args.seq},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": sample + "; oracle/gla_oracle.py (NumPy restatement of glasp, f64)"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2507_01004_b200 import distributed as zd
+
+    H, L, D, C = args.heads, args.seq, args.dim, args.chunk
+    gen = torch.Generator(device=dev).manual_seed(args.seed * 1000 + rank)
+
+    def uni(shape, lo, hi, dt):
+        return (torch.rand(shape, device=dev, generator=gen) * (hi - lo) + lo).to(dt)
+
+    q = uni((H, L, D), -1, 1, torch.bfloat16)
+    k = uni((H, L, D), -1, 1, torch.bfloat16)
+    v = uni((H, L, D), -1, 1, torch.bfloat16)
+    g = uni((H, L, D), math.log(0.9), math.log(0.999), torch.float32)
+    do = uni((H, L, D), -1, 1, torch.bfloat16)
+    comm = zd.AllScanP2P(H, D, D) if world > 1 else None
+    layer = zd.ZecoRank(H, L, D, C, torch.bfloat16, comm=comm, num_blocks=args.blocks)
+    assert layer.shard.fast, "fused tcgen05 path not selected"
+    o = torch.empty_like(q)
+    grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty_like(g))
+    stream = torch.cuda.current_stream()
+
+    phases = ["fwd_local", "fwd_allscan", "fwd_output", "bwd_local", "bwd_allscan", "bwd_output"]
+
+    def step(evs=None):
+        def mark(i):
+            if evs is not None:
+                evs[i].record(stream)
+        mark(0)
+        s_loc, g_tot = layer.shard.fwd_local(k, v, g)
+        mark(1)
+        prev = None
+        if comm is not None:
+            recv, _ = comm(s_loc, g_tot, args.blocks, 0)
+            prev = recv if rank > 0 else None
+        mark(2)
+        layer.shard.fwd_output(q, k, v, g, prev, out=o)
+        mark(3)
+        ds0 = layer.shard.bwd_local(q, g, do)
+        mark(4)
+        ds_next = None
+        if comm is not None:
+            recv_b, _ = comm(ds0, g_tot, args.blocks, 1)
+            ds_next = recv_b if rank < world - 1 else None
+        mark(5)
+        layer.shard.bwd_output(q, k, v, g, do, prev, ds_next, grads=grads)
+        mark(6)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    per_phase = {p: statistics.mean(e[j].elapsed_time(e[j + 1]) for e in evs) for j, p in enumerate(phases)}
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * L / (ms_step / 1e3)
+
+    # ---- end to end through the C-ABI with pinned HOST buffers (copies inside the timed region)
+    host_in = [x.cpu().pin_memory() for x in (q, k, v, g, do)]
+    host_out = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (o,) + grads]
+    dev_in = [torch.empty_like(x) for x in (q, k, v, g, do)]
+    h2d = sum(x.numel() * x.element_size() for x in host_in)
+    d2h = sum(x.numel() * x.element_size() for x in host_out)
+
+    def e2e_step():
+        for hsrc, dd in zip(host_in, dev_in):
+            dd.copy_(hsrc, non_blocking=True)
+        qq, kk, vv, gg, dd_o = dev_in
+        s_loc, g_tot = layer.shard.fwd_local(kk, vv, gg)
+        prev = None
+        if comm is not None:
+            recv, _ = comm(s_loc, g_tot, args.blocks, 0)
+            prev = recv if rank > 0 else None
+        layer.shard.fwd_output(qq, kk, vv, gg, prev, out=o)
+        ds0 = layer.shard.bwd_local(qq, gg, dd_o)
+        ds_next = None
+        if comm is not None:
+            rb, _ = comm(ds0, g_tot, args.blocks, 1)
+            ds_next = rb if rank < world - 1 else None
+        layer.shard.bwd_output(qq, kk, vv, gg, dd_o, prev, ds_next, grads=grads)
+        for hdst, src in zip(host_out, (o,) + grads):
+            hdst.copy_(src, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- roofline of the dominant kernel (bwd_out_kernel) and of the whole step
+    hbm, tc_peak, peak_kind = peaks()
+    fwd_b, bwd_b = bytes_per_token_head(D, D)
+    fwd_f, bwd_f = flops_per_token_head(C, D, D)
+    units = H * L
+    dom = max(("fwd_output", "bwd_output", "fwd_local", "bwd_local"), key=lambda p: per_phase[p])
+    dom_bytes = {"fwd_output": fwd_b, "bwd_output": bwd_b, "fwd_local": 2 * D + 2 * D + 4 * D,
+                 "bwd_local": 2 * D + 2 * D + 4 * D}[dom] * units
+    dom_ms = per_phase[dom]
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    step_bytes = (fwd_b + bwd_b) * units
+    step_flops = (fwd_f + bwd_f) * units
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded U(-1,1) q/k/v/dO, g~U(log .9, log .999))",
+        "config": {"workload": "cfg2: GLA layer fwd+bwd, H=16, d_k=d_v=128, 16384 tokens/GPU, chunk 64",
+                   "heads": H, "head_dim": D, "chunk": C, "tokens_per_gpu": L, "global_tokens": world * L,
+                   "allscan_blocks": args.blocks, "parallelism": f"zeco-sp{world}",
+                   "l2": "inputs 384 MiB per GPU > 126 MiB L2 (no flush needed)"},
+        "per_gpu_tokens_per_s": L / (ms_step / 1e3),
+        "phase_ms": {p: round(per_phase[p], 5) for p in phases},
+        "roofline": {"kernel": {"fwd_output": "fwd_out_kernel", "bwd_output": "bwd_out_kernel",
+                                "fwd_local": "seg_state_kernel<0>+fwd_scan", "bwd_local": "seg_state_kernel<1>+bwd_scan"}[dom],
+                     "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": load_traffic(), "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": dom_bytes},
+        "roofline_step": {"bound": "hbm", "algorithmic_bytes": step_bytes,
+                          "achieved_gbs": step_bytes / (ms_step / 1e3) / 1e9,
+                          "frac": step_bytes / (ms_step / 1e3) / 1e9 / hbm,
+                          "tflops": step_flops / (ms_step / 1e3) / 1e12,
+                          "tensor_frac": step_flops / (ms_step / 1e3) / 1e12 / tc_peak},
+        "e2e": {"value": world * L / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "gpu_launches": args.steps * (6 + (4 if world > 1 else 0)),
+        "clocks": clk.summary(),
+    }
+    if world > 1:
+        line["allscan_us"] = {"fwd": per_phase["fwd_allscan"] * 1e3, "bwd": per_phase["bwd_allscan"] * 1e3}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        workers = max(1, min(cores, H))
+        L_sample = 512
+        t_cpu = cpu_sample(H, L_sample, D, C, workers)
+        line["cpu_baseline"] = {"value": L_sample / t_cpu, "unit": UNIT, "cores": workers, "kind": "port",
+                                "sample": f"oracle/gla_oracle.py f64 ZeCO fwd+bwd, all {H} heads x {L_sample} "
+                                          f"tokens, d={D}, {workers} processes"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

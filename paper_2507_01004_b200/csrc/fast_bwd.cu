@@ -36,7 +36,9 @@ constexpr int BO_OFF_VEC = BO_OFF_DPM + T * T * 2;
 constexpr int BO_OFF_X = BO_OFF_VEC + BO_NS * 2 * D * 4;
 constexpr int BO_OFF_BAR = BO_OFF_X + 4096;
 constexpr size_t BO_SMEM = 1024 + BO_OFF_BAR + 256;
-constexpr uint32_t BC_DQ = 0, BC_DK = 64, BC_DV = 128, BC_QDO = 192, BC_A = 320, BC_DPC = 384;
+// TMEM columns.  Scores (lanes 0-15 of each quarter) and dP (lanes 16-31) share one M=64 column block;
+// LB holds d = logb - r per (channel lane, token column), double buffered, written by the prep warps.
+constexpr uint32_t BC_DQ = 0, BC_DK = 64, BC_DV = 128, BC_QDO = 192, BC_SC = 320, BC_LB = 384;
 
 __global__ void __launch_bounds__(BO_THREADS, 1)
     bwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -74,7 +76,8 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   uint64_t* grads_empty = sc_full + 6;
   uint64_t* sp_full = sc_full + 7;
   uint64_t* sp_empty = sc_full + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sc_full + 9);
+  uint64_t* lb_empty = sc_full + 9;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sc_full + 11);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int hh = blockIdx.x / nseg, s = blockIdx.x % nseg;
@@ -98,6 +101,8 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
     mbar_init(grads_empty, 256);
     mbar_init(sp_full, 1);
     mbar_init(sp_empty, 1);
+    mbar_init(&lb_empty[0], 256);
+    mbar_init(&lb_empty[1], 256);
     fence_barrier_init();
   }
   if (warp == 0) {
@@ -158,8 +163,9 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {  // scores and dP, K = 128 channels
           const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
-          mma_bf16_ss(tbase + BC_A, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_sc, kk > 0);
-          mma_bf16_ss(tbase + BC_DPC, sdesc(da + off, 16, 1024), sdesc(va + off, 16, 1024), id_sc, kk > 0);
+          mma_bf16_ss(tbase + BC_SC, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_sc, kk > 0);
+          mma_bf16_ss(tbase + (16u << 16) + BC_SC, sdesc(da + off, 16, 1024), sdesc(va + off, 16, 1024), id_sc,
+                      kk > 0);
         }
         mma_commit(sc_full);
         mbar_wait(qdo_empty, (m & 1) ^ 1);
@@ -202,53 +208,46 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       }
     }
   } else if (warp >= 8) {
-    // ---------------- prep: logb, r, Qh / Kh in place (g read straight from global)
-    const int t = tid - 256;
-    const int cp = t & 63, rh = t >> 6;
+    // ---------------- prep: one thread per channel c (warp w handles TMEM lane quarter w%4):
+    //   logb over the 64 tile rows, r = logb[31], gamma = logb[63], Qh / Kh in place,
+    //   d = logb - r -> TMEM (double buffered) for the epilogue
+    const int c = tid - 256;
+    const int quarter = c >> 5;
+    const uint32_t coff = (c >> 6) * PANEL + (c & 7) * 2, cchk = (c & 63) >> 3;
+    constexpr float LOG2E = 1.4426950408889634f;
     for (int m = 0; m < nt; ++m) {
       const int st = m % BO_NS, ph = (m / BO_NS) & 1;
       const int n = t1 - 1 - m;
       uint8_t* sb = smem + st * BO_STAGE;
-      float2 lb[32];  // gates, then their in-chunk prefix (in place)
-      const float* gp = g + ((long long)row0 + n * T + 32 * rh) * D + 2 * cp;
+      float lb[64];
+      const float* gp = g + ((long long)row0 + n * T) * D + c;
 #pragma unroll
-      for (int r = 0; r < 32; ++r) lb[r] = __ldg(reinterpret_cast<const float2*>(gp + r * D));
-      float run0 = 0.f, run1 = 0.f;
+      for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        run0 += lb[r].x;
-        run1 += lb[r].y;
-        lb[r] = make_float2(run0, run1);
-      }
+      for (int r = 1; r < 64; ++r) lb[r] += lb[r - 1];
+      const float rr = lb[31];
+#pragma unroll
+      for (int r = 0; r < 64; ++r) lb[r] -= rr;
       mbar_wait(&full[st], ph);
-      if (rh == 0) xa[cp] = make_float2(run0, run1);
-      named_bar(1, 128);
-      const float2 half = xa[cp];
-      float off0 = 0.f, off1 = 0.f;
-      if (rh == 1) {
-        off0 = half.x;
-        off1 = half.y;
-        xb[cp] = make_float2(half.x + run0, half.y + run1);
-      }
-      named_bar(1, 128);
-      if (rh == 0) {
-        const float2 gam = xb[cp];
-        vgam[st * D + 2 * cp] = gam.x;
-        vgam[st * D + 2 * cp + 1] = gam.y;
-        vr[st * D + 2 * cp] = half.x;
-        vr[st * D + 2 * cp + 1] = half.y;
-      }
-      constexpr float LOG2E = 1.4426950408889634f;
+      vgam[st * D + c] = lb[63] + rr;
+      vr[st * D + c] = rr;
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const float d0 = (lb[r].x + off0 - half.x) * LOG2E, d1 = (lb[r].y + off1 - half.y) * LOG2E;
-        const uint32_t o = pair_off(32 * rh + r, cp, PANEL);
-        uint32_t* pq = reinterpret_cast<uint32_t*>(sb + o);
-        uint32_t* pk = reinterpret_cast<uint32_t*>(sb + TILE_BF16 + o);
-        const float2 qv = unpack_bf16(*pq), kv = unpack_bf16(*pk);
-        *pq = pack_bf16(qv.x * fast_exp2(d0), qv.y * fast_exp2(d1));
-        *pk = pack_bf16(kv.x * fast_exp2(-d0), kv.y * fast_exp2(-d1));
+      for (int r = 0; r < 64; ++r) {
+        const uint32_t o = coff + sw128(r, cchk);
+        __nv_bfloat16* pq = reinterpret_cast<__nv_bfloat16*>(sb + o);
+        __nv_bfloat16* pk = reinterpret_cast<__nv_bfloat16*>(sb + TILE_BF16 + o);
+        const float e = fast_exp2(lb[r] * LOG2E), ie = fast_exp2(-lb[r] * LOG2E);
+        *pq = __float2bfloat16_rn(__bfloat162float(*pq) * e);
+        *pk = __float2bfloat16_rn(__bfloat162float(*pk) * ie);
       }
+      mbar_wait(&lb_empty[m & 1], ((m >> 1) & 1) ^ 1);
+      tc_fence_after();
+      {
+        const uint32_t la = taddr(tbase, 32 * quarter, BC_LB + 64 * (m & 1));
+        tmem_st32(la, *reinterpret_cast<const float(*)[32]>(&lb[0]));
+        tmem_st32(la + 32, *reinterpret_cast<const float(*)[32]>(&lb[32]));
+      }
+      tc_fence_before();
       fence_proxy_async();
       mbar_arrive(&prep[st]);
     }
@@ -262,49 +261,55 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const float cgr = ds_next ? expf(cumGr[(hh * nseg + s) * D + c]) : 0.f;
       const float cg = s_prev ? expf(cumG[(hh * nseg + s) * D + c]) : 0.f;
       const float eg = expf(gamseg[(hh * nseg + s) * D + c]);
-      const float* pn = ds_next ? ds_next + ((long long)hh * D + c) * D + 64 * ch : nullptr;
-      const float* pp = s_prev ? s_prev + ((long long)hh * D + c) * D + 64 * ch : nullptr;
+      const long long pidx = ((long long)hh * D + c) * D + 64 * ch;
       float rho = 0.f;
 #pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        float dd = Dend[sidx + j];
-        if (pn) dd += cgr * pn[j];
-        Dst[j] = dd;
-        float si = Sin[sidx + j];
-        if (pp) si += cg * pp[j];
-        const float se = eg * si + dS[sidx + j];  // fp32 forward state at the segment end
-        rho += se * dd;
+      for (int j = 0; j < 64; j += 4) {
+        float4 dd = *reinterpret_cast<const float4*>(Dend + sidx + j);
+        float4 si = *reinterpret_cast<const float4*>(Sin + sidx + j);
+        const float4 ds = *reinterpret_cast<const float4*>(dS + sidx + j);
+        if (ds_next) {
+          const float4 a = *reinterpret_cast<const float4*>(ds_next + pidx + j);
+          dd.x += cgr * a.x; dd.y += cgr * a.y; dd.z += cgr * a.z; dd.w += cgr * a.w;
+        }
+        if (s_prev) {
+          const float4 a = *reinterpret_cast<const float4*>(s_prev + pidx + j);
+          si.x += cg * a.x; si.y += cg * a.y; si.z += cg * a.z; si.w += cg * a.w;
+        }
+        Dst[j] = dd.x; Dst[j + 1] = dd.y; Dst[j + 2] = dd.z; Dst[j + 3] = dd.w;
+        // fp32 forward state at the segment end: e^{gam_s} S_in + dS_s
+        rho += (eg * si.x + ds.x) * dd.x + (eg * si.y + ds.y) * dd.y + (eg * si.z + ds.z) * dd.z +
+               (eg * si.w + ds.w) * dd.w;
       }
       xrho[ch * D + c] = rho;
     }
     named_bar(2, 256);
     if (ch == 0) xr[c] = xrho[c] + xrho[D + c];
+    const uint32_t cbase = (c >> 6) * PANEL + (c & 7) * 2;
+    const uint32_t cchunk = (c & 63) >> 3;
     for (int m = 0; m < nt; ++m) {
       const int st = m % BO_NS, ph = (m / BO_NS) & 1;
       const int n = t1 - 1 - m;
-      // (a) masked scores / dP -> bf16 operands
+      // (a) masked scores (lanes 0-15) and dP (lanes 16-31) -> bf16 operands
       mbar_wait(sc_full, m & 1);
       tc_fence_after();
-#pragma unroll
-      for (int which = 0; which < 2; ++which) {
+      {
         float a[32];
-        tmem_ld32(taddr(tbase, 32 * qd, (which ? BC_DPC : BC_A) + 32 * ch), a);
-        uint8_t* dstbuf = which ? dpm_buf : am_buf;
-        if (lane < 16) {
-          const int i = 16 * qd + lane;
+        tmem_ld32(taddr(tbase, 32 * qd, BC_SC + 32 * ch), a);
+        const int i = 16 * qd + (lane & 15);
+        uint8_t* dstbuf = lane < 16 ? am_buf : dpm_buf;
 #pragma unroll
-          for (int mm = 0; mm < 4; ++mm) {
-            const int j0 = 32 * ch + 8 * mm;
-            float x[8];
+        for (int mm = 0; mm < 4; ++mm) {
+          const int j0 = 32 * ch + 8 * mm;
+          float x[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) x[u] = (j0 + u <= i) ? a[8 * mm + u] : 0.f;
-            uint4 w;
-            w.x = pack_bf16(x[0], x[1]);
-            w.y = pack_bf16(x[2], x[3]);
-            w.z = pack_bf16(x[4], x[5]);
-            w.w = pack_bf16(x[6], x[7]);
-            *reinterpret_cast<uint4*>(dstbuf + sw128(i, 4 * ch + mm)) = w;
-          }
+          for (int u = 0; u < 8; ++u) x[u] = (j0 + u <= i) ? a[8 * mm + u] : 0.f;
+          uint4 w;
+          w.x = pack_bf16(x[0], x[1]);
+          w.y = pack_bf16(x[2], x[3]);
+          w.z = pack_bf16(x[4], x[5]);
+          w.w = pack_bf16(x[6], x[7]);
+          *reinterpret_cast<uint4*>(dstbuf + sw128(i, 4 * ch + mm)) = w;
         }
       }
       fence_proxy_async();
@@ -345,57 +350,46 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       mbar_arrive(qdo_empty);
       // (d) epilogue: thread owns channel c, tokens [32*ch, 32*ch+32) of the tile.
       //     pass 1: T = sum of da over my tokens (da = Qh dq_raw - Kh dk_raw needs no exponentials)
-      //     pass 2 (token order): logb, E, dq/dk/dv stores, dg_i = base - prefix_{<i}(da)
+      //     pass 2 (token order): E = e^{d}, dq/dk/dv stores, dg_i = base - prefix_{<i}(da)
       mbar_wait(grads_full, m & 1);
       tc_fence_after();
       const uint8_t* sb = smem + st * BO_STAGE;
-      const uint32_t cbase = (c >> 6) * PANEL + (c & 7) * 2;
-      const uint32_t cchunk = (c & 63) >> 3;
+      const uint32_t cols = 32 * ch;
+      const uint32_t lbcol = BC_LB + 64 * (m & 1) + cols;
       float tsum = 0.f;
-#pragma unroll
+#pragma unroll 1
       for (int q8 = 0; q8 < 4; ++q8) {
         float gq[8], gk[8];
-        tmem_ld8(taddr(tbase, 32 * qd, BC_DQ + 32 * ch + 8 * q8), gq);
-        tmem_ld8(taddr(tbase, 32 * qd, BC_DK + 32 * ch + 8 * q8), gk);
+        tmem_ld8(taddr(tbase, 32 * qd, BC_DQ + cols + 8 * q8), gq);
+        tmem_ld8(taddr(tbase, 32 * qd, BC_DK + cols + 8 * q8), gk);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const uint32_t o = cbase + sw128(32 * ch + 8 * q8 + u, cchunk);
+          const uint32_t o = cbase + sw128(cols + 8 * q8 + u, cchunk);
           const float qh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + o));
           const float kh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + TILE_BF16 + o));
           tsum += qh * gq[u] - kh * gk[u];
         }
       }
-      // logb of my first token needs the sum of the gates before it (upper half: rows 0..31 of the tile)
-      const float* gp = g + ((long long)row0 + n * T + 32 * ch) * D + c;
-      float gsum = 0.f;
-      if (ch == 0) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) gsum += __ldg(gp + (long long)i * D);
-        xtot[c] = gsum;
-      }
       xcarry[ch * D + c] = tsum;
       named_bar(2, 256);
       const float rho_end = xr[c];
       const float t_upper = xcarry[D + c], t_lower = xcarry[c];
-      // dg_i = rho_{n+1} + sum_{i' >= i} da  ->  base = rho + (da of my half and every later half)
+      // dg_i = rho_{n+1} + sum_{i' >= i in tile} da_i'
       float base = rho_end + (ch == 0 ? t_lower + t_upper : t_upper);
-      float lb = ch ? xtot[c] : 0.f;
-      const long long tok0 = (long long)row0 + n * T + 32 * ch;
+      const long long tok0 = (long long)row0 + n * T + cols;
       constexpr float LOG2E = 1.4426950408889634f;
-#pragma unroll
+#pragma unroll 1
       for (int q8 = 0; q8 < 4; ++q8) {
-        float gq[8], gk[8], gv8[8], gg[8];
-        tmem_ld8(taddr(tbase, 32 * qd, BC_DQ + 32 * ch + 8 * q8), gq);
-        tmem_ld8(taddr(tbase, 32 * qd, BC_DK + 32 * ch + 8 * q8), gk);
-        tmem_ld8(taddr(tbase, 32 * qd, BC_DV + 32 * ch + 8 * q8), gv8);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) gg[u] = __ldg(gp + (long long)(8 * q8 + u) * D);
+        float gq[8], gk[8], gv8[8], dl[8];
+        tmem_ld8(taddr(tbase, 32 * qd, BC_DQ + cols + 8 * q8), gq);
+        tmem_ld8(taddr(tbase, 32 * qd, BC_DK + cols + 8 * q8), gk);
+        tmem_ld8(taddr(tbase, 32 * qd, BC_DV + cols + 8 * q8), gv8);
+        tmem_ld8(taddr(tbase, 32 * qd, lbcol + 8 * q8), dl);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int i = 8 * q8 + u;
-          lb += gg[u];
-          const float dlt = (lb - r_c) * LOG2E;
-          const uint32_t o = cbase + sw128(32 * ch + i, cchunk);
+          const float dlt = dl[u] * LOG2E;
+          const uint32_t o = cbase + sw128(cols + i, cchunk);
           const float qh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + o));
           const float kh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + TILE_BF16 + o));
           dq[(tok0 + i) * D + c] = __float2bfloat16_rn(gq[u] * fast_exp2(dlt));
@@ -407,8 +401,9 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(grads_empty);
+      mbar_arrive(&lb_empty[m & 1]);
       mbar_arrive(&empty[st]);  // stage reads (Qh, Kh) done
-      named_bar(2, 256);        // everyone has read xr / xcarry / xtot of this tile
+      named_bar(2, 256);        // everyone has read xr / xcarry of this tile
       if (ch == 0) xr[c] = rho_end + t_lower + t_upper;  // rho at the start of this tile
     }
   }

@@ -60,6 +60,18 @@ __global__ void __launch_bounds__(128) selftest_mma_kernel(const __nv_bfloat16* 
       else bd = sdesc(smem_u32(sb) + (kk / 4) * b_rows * 128 + (kk % 4) * 32, 16, 1024);
       mma_bf16_ss(d_tmem, ad, bd, idesc, kk > 0);
     }
+    if (M == 64 && lane_off == 16) {
+      // a second M=64 tile at lane offset 0 in the SAME columns: it must not disturb lanes
+      // 16..31 of each quarter (the kernels pack two M=64 accumulators this way)
+      for (int kk = 0; kk < K / 16; ++kk) {
+        uint64_t ad, bd;
+        if (a_mn) ad = sdesc(smem_u32(sa) + kk * 16 * 128, a_rows * 128, 1024);
+        else ad = sdesc(smem_u32(sa) + (kk / 4) * a_rows * 128 + (kk % 4) * 32, 16, 1024);
+        if (b_mn) bd = sdesc(smem_u32(sb) + kk * 16 * 128, b_rows * 128, 1024);
+        else bd = sdesc(smem_u32(sb) + (kk / 4) * b_rows * 128 + (kk % 4) * 32, 16, 1024);
+        mma_bf16_ss(tbase, ad, bd, idesc, 0u);
+      }
+    }
     mma_commit(&bar);
   }
   mbar_wait(&bar, 0);

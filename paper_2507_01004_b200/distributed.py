@@ -1,0 +1,151 @@
+"""One-process-per-GPU ZeCO (SPMD form of glasp/engine.py:218-237, 348-364).
+
+``AllScanP2P`` is the product All-Scan: each rank's kernel stores its scanned
+state blocks straight into the successor's inbox over NVLink (peer memory
+mapped with CUDA IPC, handles exchanged once through torch.distributed) and
+raises a per-block flag; no NCCL call on the data path (csrc/allscan.cu).
+
+``AllScanNCCL`` (send/recv chain) and ``lasp2_states`` (all-gather of states +
+decay-weighted reduction, glasp/engine.py:165-173) are the baselines the paper
+compares against; they are kept only for measurement.
+
+``ZecoRank`` strings the per-rank kernels and the collective together for one
+GLA layer forward + backward; ``ledger`` counts elements per primitive like the
+reference's VolumeLedger contract.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from collections import defaultdict
+
+import torch
+import torch.distributed as dist
+
+from . import _native, ops
+from .errors import ConfigError
+
+
+class AllScanP2P:
+    """In-kernel NVLink chain All-Scan between the ranks of ``group`` (FWD: 0 -> P-1, BWD: P-1 -> 0)."""
+
+    def __init__(self, heads, key_dim, value_dim, group=None, max_blocks=16, rank=None, world=None):
+        self.group = group
+        self.rank = dist.get_rank(group) if rank is None else rank
+        self.world = dist.get_world_size(group) if world is None else world
+        self.shape = (heads, key_dim, value_dim)
+        lib = _native.load()
+        h = ctypes.c_void_p()
+        _native.check(lib.zgla_allscan_create(self.rank, self.world, heads, key_dim, value_dim, max_blocks,
+                                              ctypes.byref(h)), "zgla_allscan_create")
+        self._h = h
+        if self.world > 1:
+            buf = (ctypes.c_char * 64)()
+            _native.check(lib.zgla_allscan_export(self._h, buf), "zgla_allscan_export")
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(buf), group=group)
+            nxt = handles[self.rank + 1] if self.rank + 1 < self.world else None
+            prv = handles[self.rank - 1] if self.rank > 0 else None
+            _native.check(lib.zgla_allscan_bind(self._h, nxt, prv), "zgla_allscan_bind")
+            dist.barrier(group=group)
+
+    def __call__(self, local: torch.Tensor, log_decay: torch.Tensor, num_blocks: int = 1, direction: int = 0):
+        """-> (recv, scanned) for this rank; fp32 [h, dk, dv] / [h, dk]."""
+        recv = torch.empty_like(local)
+        scanned = torch.empty_like(local)
+        _native.call("zgla_allscan_run", self._h, num_blocks, direction, ops._p(local.contiguous()),
+                     ops._p(log_decay.contiguous()), ops._p(recv), ops._p(scanned), ops._stream())
+        return recv, scanned
+
+    def bytes_sent(self) -> int:
+        return int(_native.load().zgla_allscan_bytes_sent(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _native.load().zgla_allscan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _scan_update(log_decay, recv, local):
+    """scanned = e^{G} (.) recv + local; thin torch glue on the (small) state tensors of the baselines."""
+    return torch.exp(log_decay)[..., None] * recv + local
+
+
+class AllScanNCCL:
+    """Baseline: All-Scan as a NCCL send/recv chain (whole state per hop, no block pipelining)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def __call__(self, local, log_decay, num_blocks=1, direction=0):
+        order = list(range(self.world)) if direction == 0 else list(range(self.world - 1, -1, -1))
+        pos = order.index(self.rank)
+        recv = torch.zeros_like(local)
+        if pos > 0:
+            dist.recv(recv, src=order[pos - 1], group=self.group)
+        scanned = _scan_update(log_decay, recv, local)
+        if pos < self.world - 1:
+            dist.send(scanned, dst=order[pos + 1], group=self.group)
+        return recv, scanned
+
+
+def lasp2_states(local, log_decay, direction=0, group=None):
+    """Baseline (LASP-2): all-gather every rank's (state, decay), then the decay-weighted reduction."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    states = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+    decays = torch.empty((world,) + tuple(log_decay.shape), dtype=log_decay.dtype, device=log_decay.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(states, local.contiguous(), group=group)
+        dist.all_gather_into_tensor(decays, log_decay.contiguous(), group=group)
+    else:  # gloo has no fused all-gather
+        dist.all_gather(list(states.unbind(0)), local.contiguous(), group=group)
+        dist.all_gather(list(decays.unbind(0)), log_decay.contiguous(), group=group)
+    order = list(range(world)) if direction == 0 else list(range(world - 1, -1, -1))
+    recv = torch.zeros_like(local)
+    for r in order:
+        if r == rank:
+            break
+        recv = _scan_update(decays[r], recv, states[r])
+    return recv, _scan_update(log_decay, recv, local)
+
+
+class ZecoRank:
+    """One rank of ZeCO sequence-parallel GLA (one layer, fwd + bwd) over ``comm``."""
+
+    def __init__(self, heads, seq_len, dim, chunk_len=64, dtype=torch.bfloat16, comm=None, num_blocks=4, sms=None):
+        self.shard = ops.ZecoShard(heads, seq_len, dim, dim, chunk_len, dtype, sms=sms)
+        self.comm = comm
+        self.K = num_blocks
+        self.world = comm.world if comm is not None else 1
+        self.rank = comm.rank if comm is not None else 0
+        self.ledger = defaultdict(int)
+        if dim % num_blocks:
+            raise ConfigError(f"num_blocks {num_blocks} does not divide key dim {dim}")
+
+    def forward(self, q, k, v, g, out=None):
+        s_loc, g_tot = self.shard.fwd_local(k, v, g)
+        prev = None
+        if self.world > 1:
+            recv, _ = self.comm(s_loc, g_tot, self.K, _native.ZGLA_FWD)
+            self.ledger[("all_scan", "sent")] += s_loc.numel() if self.rank < self.world - 1 else 0
+            prev = recv if self.rank > 0 else None
+        self._prev, self._g_tot = prev, g_tot
+        return self.shard.fwd_output(q, k, v, g, prev, out=out)
+
+    def backward(self, q, k, v, g, d_out, grads=None):
+        ds0 = self.shard.bwd_local(q, g, d_out)
+        ds_next = None
+        if self.world > 1:
+            recv, _ = self.comm(ds0, self._g_tot, self.K, _native.ZGLA_BWD)
+            self.ledger[("all_scan", "sent")] += ds0.numel() if self.rank > 0 else 0
+            ds_next = recv if self.rank < self.world - 1 else None
+        return self.shard.bwd_output(q, k, v, g, d_out, self._prev, ds_next, grads=grads)

@@ -1,0 +1,72 @@
+"""CPU-side checks of the C ABI: the in-tree library loads and exports every entry
+point declared in include/zeco_gla.h (no compute calls: there is no GPU here)."""
+
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "zeco_gla.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(zgla_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_entry_points():
+    syms = header_symbols()
+    for required in ("zgla_zeco_fwd_local", "zgla_zeco_fwd_output", "zgla_zeco_bwd_local", "zgla_zeco_bwd_output",
+                     "zgla_allscan_local", "zgla_allscan_run", "zgla_local_state_scan", "zgla_backward"):
+        assert required in syms
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2507_01004_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("library not built (run make)")
+    lib = _native.load()
+    missing = [s for s in header_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    # the ctypes signature table covers the header too
+    assert set(header_symbols()) <= set(_native.EXPORTED)
+
+
+def test_version_and_error_string_without_gpu():
+    from paper_2507_01004_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("library not built (run make)")
+    lib = _native.load()
+    assert b"sm_100a" in lib.zgla_version()
+    assert isinstance(lib.zgla_last_error(), bytes)
+
+
+def test_status_codes_map_to_reference_exceptions():
+    from paper_2507_01004_b200 import _native, errors
+
+    for code, exc in ((-1, errors.DimsError), (-2, errors.DomainError), (-3, errors.LayoutError),
+                      (-4, errors.ConfigError), (-5, errors.StateError), (-6, errors.DeadlockError)):
+        if not os.path.exists(_native.LIB_PATH):
+            pytest.skip("library not built")
+        with pytest.raises(exc):
+            _native.check(code, "probe")
+
+
+def test_invalid_shapes_rejected_before_any_launch():
+    """Argument validation happens on the host side of the C ABI (no device needed)."""
+    import ctypes
+
+    from paper_2507_01004_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("library not built")
+    lib = _native.load()
+    bad = _native.Shape(heads=2, key_dim=4, value_dim=4, chunk_len=3, seq_len=8, dtype=_native.ZGLA_F64)
+    assert lib.zgla_workspace_bytes(ctypes.byref(bad)) == -1           # chunk does not divide L
+    assert lib.zgla_zeco_workspace_bytes(ctypes.byref(bad), 148) == -1
+    ok = _native.Shape(heads=16, key_dim=128, value_dim=128, chunk_len=64, seq_len=16384, dtype=_native.ZGLA_BF16)
+    assert lib.zgla_zeco_workspace_bytes(ctypes.byref(ok), 148) > 0
+    assert lib.zgla_allscan_local(2, 1, 4, 4, _native.ZGLA_F32, 3, 0, None, None, None, None, None) == -4
