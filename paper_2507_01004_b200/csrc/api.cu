@@ -8,6 +8,9 @@
 
 namespace zgla {
 
+unsigned long long* g_trace_buf = nullptr;
+int g_trace_cta = 0;
+
 static thread_local char g_err[512] = "";
 
 void set_error(const char* msg) {
@@ -46,6 +49,12 @@ using namespace zgla;
 extern "C" int zgla_check_launch_impl(const char* where) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, where);
+  return ZGLA_OK;
+}
+
+extern "C" int zgla_set_trace(void* dev_buf, int cta) {
+  g_trace_buf = reinterpret_cast<unsigned long long*>(dev_buf);
+  g_trace_cta = cta;
   return ZGLA_OK;
 }
 

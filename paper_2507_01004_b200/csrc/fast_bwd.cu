@@ -43,12 +43,14 @@ constexpr uint32_t BC_DQ = 0, BC_DK = 64, BC_DV = 128, BC_QDO = 192, BC_SC = 320
 __global__ void __launch_bounds__(BO_THREADS, 1)
     bwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-                   const __grid_constant__ CUtensorMap tm_sp, const float* __restrict__ g, long long L, int nseg,
+                   const __grid_constant__ CUtensorMap tm_sp, const __grid_constant__ CUtensorMap tm_g,
+                   const float* __restrict__ g, long long L, int nseg,
                    int ntiles, const float* __restrict__ Sin, const float* __restrict__ cumG,
                    const float* __restrict__ dS, const float* __restrict__ gamseg, const float* __restrict__ s_prev,
                    const float* __restrict__ Dend, const float* __restrict__ cumGr,
                    const float* __restrict__ ds_next, __nv_bfloat16* __restrict__ dq, __nv_bfloat16* __restrict__ dk,
-                   __nv_bfloat16* __restrict__ dv, float* __restrict__ dg) {
+                   __nv_bfloat16* __restrict__ dv, float* __restrict__ dg, unsigned long long* trace,
+                   int trace_cta) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sp_buf = smem + BO_OFF_SP;
@@ -85,6 +87,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   seg_range(s, nseg, ntiles, t0, t1);
   const int nt = t1 - t0;
   const int row0 = (int)(hh * L);
+  unsigned long long* tr = (trace != nullptr && (int)blockIdx.x == trace_cta) ? trace : nullptr;
 
   if (tid == 0) {
     for (int i = 0; i < BO_NS; ++i) {
@@ -122,7 +125,24 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_do);
       tma_prefetch_desc(&tm_sp);
-      for (int m = 0; m < nt; ++m) {
+      for (int i = 0; i < nt + PF_DIST; ++i) {
+        if (PF_DIST > 0 && i < nt) {
+          const int r = row0 + (t1 - 1 - i) * T;
+          tma_prefetch_2d(&tm_q, 0, r);
+          tma_prefetch_2d(&tm_q, 64, r);
+          tma_prefetch_2d(&tm_k, 0, r);
+          tma_prefetch_2d(&tm_k, 64, r);
+          tma_prefetch_2d(&tm_v, 0, r);
+          tma_prefetch_2d(&tm_v, 64, r);
+          tma_prefetch_2d(&tm_do, 0, r);
+          tma_prefetch_2d(&tm_do, 64, r);
+          tma_prefetch_2d(&tm_g, 0, r);
+          const int rs = (hh * ntiles + (t1 - 1 - i)) * D;
+          tma_prefetch_2d(&tm_sp, 0, rs);
+          tma_prefetch_2d(&tm_sp, 64, rs);
+        }
+        const int m = i - PF_DIST;
+        if (m < 0) continue;
         const int st = m % BO_NS, ph = (m / BO_NS) & 1;
         const int n = t1 - 1 - m;
         uint8_t* sb = smem + st * BO_STAGE;
@@ -142,6 +162,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         const int rs = (hh * ntiles + n) * D;
         tma_load_2d(sp_buf, &tm_sp, sp_full, 0, rs);
         tma_load_2d(sp_buf + SPANEL, &tm_sp, sp_full, 64, rs);
+        ZTRACE(tr, 0, m);
       }
     }
   } else if (warp == 13) {
@@ -168,6 +189,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
                       kk > 0);
         }
         mma_commit(sc_full);
+        ZTRACE(tr, 2, m);
         mbar_wait(qdo_empty, (m & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
@@ -179,6 +201,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         mbar_wait(grads_empty, (m & 1) ^ 1);
         mbar_wait(sp_full, m & 1);
         tc_fence_after();
+        ZTRACE(tr, 3, m);
 #pragma unroll
         for (int kk = 0; kk < T / 16; ++kk)  // dq^T = Kh^T dPm^T
           mma_bf16_ss(tbase + BC_DQ, sdesc(ka + kk * 2048, PANEL, 1024), sdesc(dpma + kk * 32, 16, 1024), id_mk,
@@ -205,6 +228,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           mma_bf16_ss(tbase + BC_DV, sdesc(dpa + kk * 2048, SPANEL, 1024), sdesc(ka + boff, 16, 1024), id_mk, 1);
         }
         mma_commit(grads_full);
+        ZTRACE(tr, 4, m);
       }
     }
   } else if (warp >= 8) {
@@ -232,13 +256,26 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       vgam[st * D + c] = lb[63] + rr;
       vr[st * D + c] = rr;
 #pragma unroll
-      for (int r = 0; r < 64; ++r) {
-        const uint32_t o = coff + sw128(r, cchk);
-        __nv_bfloat16* pq = reinterpret_cast<__nv_bfloat16*>(sb + o);
-        __nv_bfloat16* pk = reinterpret_cast<__nv_bfloat16*>(sb + TILE_BF16 + o);
-        const float e = fast_exp2(lb[r] * LOG2E), ie = fast_exp2(-lb[r] * LOG2E);
-        *pq = __float2bfloat16_rn(__bfloat162float(*pq) * e);
-        *pk = __float2bfloat16_rn(__bfloat162float(*pk) * ie);
+      for (int r0 = 0; r0 < 64; r0 += 8) {  // batches: all loads, then all stores (smem may alias)
+        __nv_bfloat16 xq[8], xk[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const uint32_t o = coff + sw128(r0 + r, cchk);
+          xq[r] = *reinterpret_cast<const __nv_bfloat16*>(sb + o);
+          xk[r] = *reinterpret_cast<const __nv_bfloat16*>(sb + TILE_BF16 + o);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float d = lb[r0 + r] * LOG2E;
+          xq[r] = __float2bfloat16_rn(__bfloat162float(xq[r]) * fast_exp2(d));
+          xk[r] = __float2bfloat16_rn(__bfloat162float(xk[r]) * fast_exp2(-d));
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const uint32_t o = coff + sw128(r0 + r, cchk);
+          *reinterpret_cast<__nv_bfloat16*>(sb + o) = xq[r];
+          *reinterpret_cast<__nv_bfloat16*>(sb + TILE_BF16 + o) = xk[r];
+        }
       }
       mbar_wait(&lb_empty[m & 1], ((m >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -250,6 +287,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       tc_fence_before();
       fence_proxy_async();
       mbar_arrive(&prep[st]);
+      if (c == 0) ZTRACE(tr, 1, m);
     }
   } else {
     // ---------------- state / epilogue warps
@@ -293,6 +331,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       // (a) masked scores (lanes 0-15) and dP (lanes 16-31) -> bf16 operands
       mbar_wait(sc_full, m & 1);
       tc_fence_after();
+      if (tid == 0) ZTRACE(tr, 5, m);
       {
         float a[32];
         tmem_ld32(taddr(tbase, 32 * qd, BC_SC + 32 * ch), a);
@@ -333,6 +372,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       }
       fence_proxy_async();
       mbar_arrive(dp_ready);
+      if (tid == 0) ZTRACE(tr, 6, m);
       // (c) D_n = e^{gam} D_{n+1} + e^{r} QDO'
       mbar_wait(qdo_full, m & 1);
       tc_fence_after();
@@ -348,11 +388,13 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(qdo_empty);
+      if (tid == 0) ZTRACE(tr, 7, m);
       // (d) epilogue: thread owns channel c, tokens [32*ch, 32*ch+32) of the tile.
       //     pass 1: T = sum of da over my tokens (da = Qh dq_raw - Kh dk_raw needs no exponentials)
       //     pass 2 (token order): E = e^{d}, dq/dk/dv stores, dg_i = base - prefix_{<i}(da)
       mbar_wait(grads_full, m & 1);
       tc_fence_after();
+      if (tid == 0) ZTRACE(tr, 8, m);
       const uint8_t* sb = smem + st * BO_STAGE;
       const uint32_t cols = 32 * ch;
       const uint32_t lbcol = BC_LB + 64 * (m & 1) + cols;
@@ -405,6 +447,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       mbar_arrive(&empty[st]);  // stage reads (Qh, Kh) done
       named_bar(2, 256);        // everyone has read xr / xcarry of this tile
       if (ch == 0) xr[c] = rho_end + t_lower + t_upper;  // rho at the start of this tile
+      if (tid == 0) ZTRACE(tr, 9, m);
     }
   }
   tc_fence_before();
@@ -421,18 +464,19 @@ int fast_bwd_output(const zgla_shape* s, int num_sms, const void* q, const void*
                     void* dv, void* dg, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
-  CUtensorMap mq, mk, mv, mdo, msp;
+  CUtensorMap mq, mk, mv, mdo, msp, mg;
   const unsigned long long rows = (unsigned long long)pl.h * pl.L;
   if (int rc = make_map(&mq, q, true, rows, D, 64, T, true)) return rc;
   if (int rc = make_map(&mk, k, true, rows, D, 64, T, true)) return rc;
   if (int rc = make_map(&mv, v, true, rows, D, 64, T, true)) return rc;
   if (int rc = make_map(&mdo, d_out, true, rows, D, 64, T, true)) return rc;
   if (int rc = make_map(&msp, w.Sp, true, (unsigned long long)pl.h * pl.ntiles * D, D, 64, D, true)) return rc;
+  if (int rc = make_map(&mg, g, false, rows, D, D, T, false)) return rc;
   cudaFuncSetAttribute(bwd_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BO_SMEM);
   bwd_out_kernel<<<pl.h * pl.nseg, BO_THREADS, BO_SMEM, st>>>(
-      mq, mk, mv, mdo, msp, (const float*)g, pl.L, pl.nseg, pl.ntiles, w.Sin, w.cumG, w.dS, w.gam,
+      mq, mk, mv, mdo, msp, mg, (const float*)g, pl.L, pl.nseg, pl.ntiles, w.Sin, w.cumG, w.dS, w.gam,
       (const float*)s_prev, w.Dend, w.cumGr, (const float*)ds_next, (__nv_bfloat16*)dq, (__nv_bfloat16*)dk,
-      (__nv_bfloat16*)dv, (float*)dg);
+      (__nv_bfloat16*)dv, (float*)dg, g_trace_buf, g_trace_cta);
   return zgla_check_launch();
 }
 

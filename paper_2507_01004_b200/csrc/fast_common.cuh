@@ -24,6 +24,7 @@ constexpr int TILE_BF16 = T * D * 2;   // 16 KiB
 constexpr int TILE_F32 = T * D * 4;    // 32 KiB
 constexpr int SPANEL = D * 128;        // one 64-column panel of a [D x D] bf16 state (16 KiB)
 constexpr int STATE_BF16 = D * D * 2;  // 32 KiB
+constexpr int PF_DIST = 0;             // tiles of L2 prefetch ahead of the smem pipeline (measured: hurts)
 
 struct Plan {
   int h, nseg, ntiles;
@@ -122,6 +123,18 @@ inline int make_map(CUtensorMap* m, const void* base, bool bf16, unsigned long l
   }
   return ZGLA_OK;
 }
+
+// ---- optional pipeline tracing (diagnostics): CTA g_trace_cta records %globaltimer per (event, tile)
+constexpr int TRACE_TILES = 512;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define ZTRACE(buf, ev, n)                                                              \
+  do {                                                                                  \
+    if ((buf) != nullptr && (n) < TRACE_TILES) (buf)[(ev) * TRACE_TILES + (n)] = gtimer(); \
+  } while (0)
 
 // ---- device helpers
 __device__ __forceinline__ void named_bar(int id, int nthreads) {

@@ -24,8 +24,9 @@ namespace fast {
 // ============================================================== K1 / K4
 constexpr int KS_NS = 3;
 constexpr int KS_STAGE = 2 * TILE_BF16 + TILE_F32;  // a, b, g = 64 KiB
-constexpr int KS_THREADS = 192;                     // 4 prep warps, TMA warp, MMA warp
-constexpr size_t KS_SMEM = 1024 + KS_NS * KS_STAGE + 2048;
+constexpr int KS_THREADS = 320;                     // 8 prep warps (2 groups), TMA warp, MMA warp
+constexpr int KS_OFF_BAR = KS_NS * KS_STAGE;
+constexpr size_t KS_SMEM = 1024 + KS_NS * KS_STAGE + 4096;
 
 template <int DIR>  // 0: forward local state (a=k, b=v, reverse walk); 1: backward (a=q, b=dO, forward walk)
 __global__ void __launch_bounds__(KS_THREADS, 1)
@@ -34,14 +35,14 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
                      float* __restrict__ out_state, float* __restrict__ out_gam) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + KS_NS * KS_STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + KS_OFF_BAR);
   uint64_t* full = bars;
   uint64_t* empty = bars + KS_NS;
   uint64_t* prep = bars + 2 * KS_NS;
-  uint64_t* done = bars + 3 * KS_NS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * KS_NS + 1);
-  float2* xa = reinterpret_cast<float2*>(smem + KS_NS * KS_STAGE + 256);
-  float2* xb = xa + 64;
+  uint64_t* gready = bars + 3 * KS_NS;  // [4] tile gammas published by one prep group for the other
+  uint64_t* done = gready + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  float* xg = reinterpret_cast<float*>(smem + KS_OFF_BAR + 256);  // [4][D]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int hh = blockIdx.x / nseg, s = blockIdx.x % nseg;
@@ -56,10 +57,11 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
       mbar_init(&empty[i], 1);
       mbar_init(&prep[i], 128);
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&gready[i], 128);
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  if (warp == 5) {
+  if (warp == 9) {
     tmem_alloc(tmem_slot, 128);
     tmem_relinquish();
   }
@@ -68,14 +70,25 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       tma_prefetch_desc(&tm_a);
       tma_prefetch_desc(&tm_b);
       tma_prefetch_desc(&tm_g);
-      for (int i = 0; i < nt; ++i) {
-        const int st = i % KS_NS, ph = (i / KS_NS) & 1;
-        const int tile = DIR == 0 ? t1 - 1 - i : t0 + i;
+      for (int i = 0; i < nt + PF_DIST; ++i) {
+        if (PF_DIST > 0 && i < nt) {
+          const int tile = DIR == 0 ? t1 - 1 - i : t0 + i;
+          const int r = row0 + tile * T;
+          tma_prefetch_2d(&tm_a, 0, r);
+          tma_prefetch_2d(&tm_a, 64, r);
+          tma_prefetch_2d(&tm_b, 0, r);
+          tma_prefetch_2d(&tm_b, 64, r);
+          tma_prefetch_2d(&tm_g, 0, r);
+        }
+        const int j = i - PF_DIST;  // tile whose shared-memory load is issued now
+        if (j < 0) continue;
+        const int st = j % KS_NS, ph = (j / KS_NS) & 1;
+        const int tile = DIR == 0 ? t1 - 1 - j : t0 + j;
         uint8_t* sa = smem + st * KS_STAGE;
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], KS_STAGE);
@@ -87,7 +100,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
         tma_load_2d(sa + 2 * TILE_BF16, &tm_g, &full[st], 0, r);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(128, 128, true, true);
       for (int i = 0; i < nt; ++i) {
@@ -106,77 +119,68 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
       mma_commit(done);
     }
   } else {
-    // prep warps: 128 threads = 64 channel pairs x 2 row halves
-    const int cp = tid & 63, rh = tid >> 6;
-    float acc0 = 0.f, acc1 = 0.f;  // running sum of gates of already-processed tiles (suffix / prefix)
-    for (int i = 0; i < nt; ++i) {
+    // prep: thread per channel c; two groups of 4 warps take alternate tiles.  The coefficient of
+    // tile i needs the sum of the gates of all tiles processed before it (acc_i); each group
+    // publishes its tile gamma early so the other group can advance its running sum.
+    const int c = tid & 127, grp = tid >> 7;
+    const uint32_t coff = (c >> 6) * PANEL + (c & 7) * 2, cchk = (c & 63) >> 3;
+    constexpr float LOG2E = 1.4426950408889634f;
+    float acc = 0.f;       // sum of gammas of tiles processed before the current one
+    float last_tot = 0.f;  // acc + gamma after my last tile
+    for (int i = grp; i < nt; i += 2) {
       const int st = i % KS_NS, ph = (i / KS_NS) & 1;
       uint8_t* sa = smem + st * KS_STAGE;
       const float* gs = reinterpret_cast<const float*>(sa + 2 * TILE_BF16);
       mbar_wait(&full[st], ph);
-      float lb0[32], lb1[32];
-      float run0 = 0.f, run1 = 0.f;
+      float lb[64];
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const float2 gv = *reinterpret_cast<const float2*>(gs + (32 * rh + r) * D + 2 * cp);
-        run0 += gv.x;
-        run1 += gv.y;
-        lb0[r] = run0;
-        lb1[r] = run1;
-      }
-      if (rh == 0) xa[cp] = make_float2(run0, run1);
-      named_bar(1, 128);
-      float off0 = 0.f, off1 = 0.f;
-      if (rh == 1) {
-        const float2 o = xa[cp];
-        off0 = o.x;
-        off1 = o.y;
-        xb[cp] = make_float2(o.x + run0, o.y + run1);
-      }
-      named_bar(1, 128);
-      const float2 tot = xb[cp];  // gamma of the tile
+      for (int r = 0; r < 64; ++r) lb[r] = gs[r * D + c];
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const float l0 = lb0[r] + off0, l1 = lb1[r] + off1;
-        float w0, w1;
-        if (DIR == 0) {
-          w0 = fast_exp(acc0 + tot.x - l0);
-          w1 = fast_exp(acc1 + tot.y - l1);
-        } else {
-          w0 = fast_exp(acc0 + l0);
-          w1 = fast_exp(acc1 + l1);
+      for (int r = 1; r < 64; ++r) lb[r] += lb[r - 1];
+      const float gam = lb[63];
+      xg[(i & 3) * D + c] = gam;
+      mbar_arrive(&gready[i & 3]);
+      if (i >= 1) {  // gamma of tile i-1 (other group)
+        mbar_wait(&gready[(i - 1) & 3], ((i - 1) >> 2) & 1);
+        acc += xg[((i - 1) & 3) * D + c];
+      }
+#pragma unroll
+      for (int r0 = 0; r0 < 64; r0 += 16) {  // batches: all loads, then all stores (smem may alias)
+        __nv_bfloat16 x[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) x[r] = *reinterpret_cast<const __nv_bfloat16*>(sa + coff + sw128(r0 + r, cchk));
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const float e = DIR == 0 ? (acc + gam - lb[r0 + r]) : (acc + lb[r0 + r]);
+          x[r] = __float2bfloat16_rn(__bfloat162float(x[r]) * fast_exp2(e * LOG2E));
         }
-        uint32_t* p = reinterpret_cast<uint32_t*>(sa + pair_off(32 * rh + r, cp, PANEL));
-        const float2 a = unpack_bf16(*p);
-        *p = pack_bf16(a.x * w0, a.y * w1);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) *reinterpret_cast<__nv_bfloat16*>(sa + coff + sw128(r0 + r, cchk)) = x[r];
       }
-      acc0 += tot.x;
-      acc1 += tot.y;
       fence_proxy_async();
       mbar_arrive(&prep[st]);
+      last_tot = acc + gam;
+      acc += gam;  // own tile; the other group's next gamma is added at the next iteration
     }
-    // epilogue: accumulator -> global (rows = d_k channels on TMEM lanes)
-    mbar_wait(done, 0);
-    tc_fence_after();
-    const int c = warp * 32 + lane;
-    float* dst = out_state + ((long long)(hh * nseg + s) * D + c) * D;
+    // epilogue (group 0): accumulator -> global (rows = d_k channels on TMEM lanes)
+    if (grp == 0) {
+      mbar_wait(done, 0);
+      tc_fence_after();
+      float* dst = out_state + ((long long)(hh * nseg + s) * D + c) * D;
 #pragma unroll
-    for (int ch = 0; ch < D / 32; ++ch) {
-      float v[32];
-      tmem_ld32(taddr(tbase, warp * 32, ch * 32), v);
+      for (int chn = 0; chn < D / 32; ++chn) {
+        float v[32];
+        tmem_ld32(taddr(tbase, warp * 32, chn * 32), v);
 #pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<float4*>(dst + ch * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(dst + chn * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
     }
-    if (rh == 0) {
-      float* gdst = out_gam + (long long)(hh * nseg + s) * D;
-      gdst[2 * cp] = acc0;
-      gdst[2 * cp + 1] = acc1;
-    }
+    if (nt > 0 && grp == ((nt - 1) & 1)) out_gam[(long long)(hh * nseg + s) * D + c] = last_tot;
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc(tbase, 128);
+  if (warp == 9) tmem_dealloc(tbase, 128);
 }
 
 // ============================================================== K2 / K5
@@ -227,9 +231,9 @@ __global__ void bwd_scan_kernel(int h, int nseg, const float* __restrict__ dD, c
 }
 
 // ============================================================== K3: forward outputs
-constexpr int FO_NS = 2;
-constexpr int FO_STAGE = 3 * TILE_BF16 + TILE_F32;  // q, k, v, g = 80 KiB
-constexpr int FO_THREADS = 448;                     // 8 state warps, 4 prep warps, TMA warp, MMA warp
+constexpr int FO_NS = 3;
+constexpr int FO_STAGE = 3 * TILE_BF16;  // q, k, v = 48 KiB (g goes straight to the prep warps' registers)
+constexpr int FO_THREADS = 448;  // 4 state warps, 8 prep warps (2 groups, alternate tiles), TMA, MMA
 constexpr int FO_OFF_SP = FO_NS * FO_STAGE;         // S' (bf16 [D][D], 2 panels)
 constexpr int FO_OFF_AM = FO_OFF_SP + STATE_BF16;   // masked scores (bf16 [64][64], 1 panel)
 constexpr int FO_OFF_VEC = FO_OFF_AM + T * T * 2;   // gamma / r per stage
@@ -241,10 +245,11 @@ constexpr uint32_t COL_KV = 0, COL_O = 128, COL_A = 256, COL_S = 320;
 
 __global__ void __launch_bounds__(FO_THREADS, 1)
     fwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g, long long L,
+                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g,
+                   const __grid_constant__ CUtensorMap tm_sp, const float* __restrict__ g, long long L,
                    int nseg, int ntiles, const float* __restrict__ Sin, const float* __restrict__ cumG,
                    const float* __restrict__ s_prev, __nv_bfloat16* __restrict__ out,
-                   __nv_bfloat16* __restrict__ sp_save) {
+                   __nv_bfloat16* __restrict__ sp_save, unsigned long long* trace, int trace_cta) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sp_buf = smem + FO_OFF_SP;
@@ -263,8 +268,8 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   uint64_t* kv_empty = a_full + 3;
   uint64_t* s_ready = a_full + 4;
   uint64_t* o_full = a_full + 5;
-  uint64_t* o_empty = a_full + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 7);
+  uint64_t* o_empty = a_full + 6;  // [2]: O is double buffered in the two lane halves
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 8);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int hh = blockIdx.x / nseg, s = blockIdx.x % nseg;
@@ -272,6 +277,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   seg_range(s, nseg, ntiles, t0, t1);
   const int nt = t1 - t0;
   const int row0 = (int)(hh * L);
+  unsigned long long* tr = (trace != nullptr && (int)blockIdx.x == trace_cta) ? trace : nullptr;
 
   if (tid == 0) {
     for (int i = 0; i < FO_NS; ++i) {
@@ -280,12 +286,13 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       mbar_init(&prep[i], 128);
     }
     mbar_init(a_full, 1);
-    mbar_init(a_done, 256);
+    mbar_init(a_done, 128);
     mbar_init(kv_full, 1);
-    mbar_init(kv_empty, 256);
-    mbar_init(s_ready, 256);
+    mbar_init(kv_empty, 128);
+    mbar_init(s_ready, 128);
     mbar_init(o_full, 1);
-    mbar_init(o_empty, 256);
+    mbar_init(&o_empty[0], 128);
+    mbar_init(&o_empty[1], 128);
     fence_barrier_init();
   }
   if (warp == 0) {
@@ -304,7 +311,19 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_g);
-      for (int n = 0; n < nt; ++n) {
+      for (int i = 0; i < nt + PF_DIST; ++i) {
+        if (PF_DIST > 0 && i < nt) {
+          const int r = row0 + (t0 + i) * T;
+          tma_prefetch_2d(&tm_q, 0, r);
+          tma_prefetch_2d(&tm_q, 64, r);
+          tma_prefetch_2d(&tm_k, 0, r);
+          tma_prefetch_2d(&tm_k, 64, r);
+          tma_prefetch_2d(&tm_v, 0, r);
+          tma_prefetch_2d(&tm_v, 64, r);
+          tma_prefetch_2d(&tm_g, 0, r);
+        }
+        const int n = i - PF_DIST;
+        if (n < 0) continue;
         const int st = n % FO_NS, ph = (n / FO_NS) & 1;
         uint8_t* sb = smem + st * FO_STAGE;
         mbar_wait(&empty[st], ph ^ 1);
@@ -316,7 +335,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         tma_load_2d(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r);
         tma_load_2d(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r);
         tma_load_2d(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r);
-        tma_load_2d(sb + 3 * TILE_BF16, &tm_g, &full[st], 0, r);
+        ZTRACE(tr, 0, n);
       }
     }
   } else if (warp == 13) {
@@ -327,6 +346,8 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       constexpr uint32_t id_kv = idesc_bf16(128, 128, true, true);
       constexpr uint32_t id_av = idesc_bf16(64, 128, false, true);
       const uint32_t spa = smem_u32(sp_buf), ama = smem_u32(am_buf);
+      const bool save_sp = sp_save != nullptr;
+      if (save_sp) tma_prefetch_desc(&tm_sp);
       for (int n = 0; n < nt; ++n) {
         const int st = n % FO_NS, ph = (n / FO_NS) & 1;
         const uint32_t qa = smem_u32(smem + st * FO_STAGE);
@@ -340,14 +361,23 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
           mma_bf16_ss(tbase + COL_A, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_sc, kk > 0);
         }
         mma_commit(a_full);
+        ZTRACE(tr, 2, n);
         mbar_wait(s_ready, n & 1);
-        mbar_wait(o_empty, (n & 1) ^ 1);
+        if (save_sp) {  // chunk-start state for the backward: async bulk store straight from smem
+          const int rs = (hh * ntiles + t0 + n) * D;
+          tma_store_2d(&tm_sp, sp_buf, 0, rs);
+          tma_store_2d(&tm_sp, sp_buf + SPANEL, 64, rs);
+          tma_store_commit();
+        }
+        const uint32_t ob = n & 1;
+        const uint32_t t_o = tbase + ((16u * ob) << 16) + COL_O;
+        mbar_wait(&o_empty[ob], ((n >> 1) & 1) ^ 1);
+        ZTRACE(tr, 11, n);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
-          mma_bf16_ss(tbase + COL_O, sdesc(qa + off, 16, 1024), sdesc(spa + kk * 2048, SPANEL, 1024), id_qs,
-                      kk > 0);
+          mma_bf16_ss(t_o, sdesc(qa + off, 16, 1024), sdesc(spa + kk * 2048, SPANEL, 1024), id_qs, kk > 0);
         }
         mbar_wait(kv_empty, (n & 1) ^ 1);
         tc_fence_after();
@@ -355,78 +385,75 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         for (int kk = 0; kk < T / 16; ++kk)
           mma_bf16_ss(tbase + COL_KV, sdesc(ka + kk * 2048, PANEL, 1024), sdesc(va + kk * 2048, PANEL, 1024),
                       id_kv, kk > 0);
+        if (save_sp) tma_store_wait_read0();  // S' may be overwritten once kv_full fires
         mma_commit(kv_full);  // also orders the S' read of the inter-chunk MMA before the next S' write
+        ZTRACE(tr, 3, n);
         mbar_wait(a_done, n & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < T / 16; ++kk)
-          mma_bf16_ss(tbase + COL_O, sdesc(ama + kk * 32, 16, 1024), sdesc(va + kk * 2048, PANEL, 1024), id_av, 1);
+          mma_bf16_ss(t_o, sdesc(ama + kk * 32, 16, 1024), sdesc(va + kk * 2048, PANEL, 1024), id_av, 1);
         mma_commit(o_full);
         mma_commit(&empty[st]);
+        ZTRACE(tr, 4, n);
       }
+      if (save_sp) tma_store_wait0();
     }
-  } else if (warp >= 8) {
-    // ---------------- prep: in-chunk log cumsum, reference point, Qh / Kh in place
-    const int t = tid - 256;
-    const int cp = t & 63, rh = t >> 6;
-    for (int n = 0; n < nt; ++n) {
+  } else if (warp >= 4) {
+    // ---------------- prep (2 groups of 4 warps, alternate tiles): one thread per channel c:
+    //                  in-chunk log cumsum over the 64 rows, r = logb[31], gamma = logb[63], Qh / Kh in place
+    const int t = tid - 128;
+    const int c = t & 127, grp = t >> 7;
+    const uint32_t coff = (c >> 6) * PANEL + (c & 7) * 2, cchk = (c & 63) >> 3;
+    constexpr float LOG2E = 1.4426950408889634f;
+    for (int n = grp; n < nt; n += 2) {
       const int st = n % FO_NS, ph = (n / FO_NS) & 1;
       uint8_t* sb = smem + st * FO_STAGE;
-      const float* gs = reinterpret_cast<const float*>(sb + 3 * TILE_BF16);
+      float lb[64];
+      const float* gp = g + ((long long)row0 + (t0 + n) * T) * D + c;
+#pragma unroll
+      for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);
+#pragma unroll
+      for (int r = 1; r < 64; ++r) lb[r] += lb[r - 1];
+      const float rr = lb[31];
       mbar_wait(&full[st], ph);
-      float lb0[32], lb1[32];
-      float run0 = 0.f, run1 = 0.f;
+      if (t == 0 || t == 128) ZTRACE(tr, 12, n);
+      vgam[st * D + c] = lb[63];
+      vr[st * D + c] = rr;
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const float2 gv = *reinterpret_cast<const float2*>(gs + (32 * rh + r) * D + 2 * cp);
-        run0 += gv.x;
-        run1 += gv.y;
-        lb0[r] = run0;
-        lb1[r] = run1;
-      }
-      if (rh == 0) xa[cp] = make_float2(run0, run1);
-      named_bar(1, 128);
-      const float2 half = xa[cp];  // logb at row 31 = the reference point r
-      float off0 = 0.f, off1 = 0.f;
-      if (rh == 1) {
-        off0 = half.x;
-        off1 = half.y;
-        xb[cp] = make_float2(half.x + run0, half.y + run1);
-      }
-      named_bar(1, 128);
-      if (rh == 0) {
-        const float2 gam = xb[cp];
-        vgam[st * D + 2 * cp] = gam.x;
-        vgam[st * D + 2 * cp + 1] = gam.y;
-        vr[st * D + 2 * cp] = half.x;
-        vr[st * D + 2 * cp + 1] = half.y;
-      }
-      constexpr float LOG2E = 1.4426950408889634f;
+      for (int r0 = 0; r0 < 64; r0 += 8) {  // batches: all loads, then all stores (smem may alias)
+        __nv_bfloat16 xq[8], xk[8];
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const float d0 = (lb0[r] + off0 - half.x) * LOG2E, d1 = (lb1[r] + off1 - half.y) * LOG2E;
-        const float e0 = fast_exp2(d0), e1 = fast_exp2(d1);
-        const float i0 = fast_exp2(-d0), i1 = fast_exp2(-d1);
-        const uint32_t o = pair_off(32 * rh + r, cp, PANEL);
-        uint32_t* pq = reinterpret_cast<uint32_t*>(sb + o);
-        uint32_t* pk = reinterpret_cast<uint32_t*>(sb + TILE_BF16 + o);
-        const float2 qv = unpack_bf16(*pq), kv = unpack_bf16(*pk);
-        *pq = pack_bf16(qv.x * e0, qv.y * e1);
-        *pk = pack_bf16(kv.x * i0, kv.y * i1);
+        for (int r = 0; r < 8; ++r) {
+          const uint32_t o = coff + sw128(r0 + r, cchk);
+          xq[r] = *reinterpret_cast<const __nv_bfloat16*>(sb + o);
+          xk[r] = *reinterpret_cast<const __nv_bfloat16*>(sb + TILE_BF16 + o);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float d = (lb[r0 + r] - rr) * LOG2E;
+          xq[r] = __float2bfloat16_rn(__bfloat162float(xq[r]) * fast_exp2(d));
+          xk[r] = __float2bfloat16_rn(__bfloat162float(xk[r]) * fast_exp2(-d));
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const uint32_t o = coff + sw128(r0 + r, cchk);
+          *reinterpret_cast<__nv_bfloat16*>(sb + o) = xq[r];
+          *reinterpret_cast<__nv_bfloat16*>(sb + TILE_BF16 + o) = xk[r];
+        }
       }
       fence_proxy_async();
       mbar_arrive(&prep[st]);
+      if (t == 0 || t == 128) ZTRACE(tr, 1, n);
     }
   } else {
-    // ---------------- state / epilogue warps (8): thread owns S[c][64*ch .. +64] (in TMEM), c = 32*qd + lane
-    const int qd = warp & 3, ch = warp >> 2;
+    // ---------------- state / epilogue warps (4): thread owns row c of the fp32 state S (in TMEM)
+    const int qd = warp;
     const int c = 32 * qd + lane;
-    const uint32_t s_addr = taddr(tbase, 32 * qd, COL_S + 64 * ch);
-    // S' = scale * S for 32 columns -> smem B operand (and the backward's copy in global memory)
-    auto write_sp = [&](const float (&v)[32], int hf, int tile_idx, float scale) {
-      uint8_t* dst = sp_buf + ch * SPANEL;
-      __nv_bfloat16* gdst =
-          sp_save ? sp_save + ((long long)(hh * ntiles + t0 + tile_idx) * D + c) * D + 64 * ch + 32 * hf : nullptr;
+    const uint32_t s_addr = taddr(tbase, 32 * qd, COL_S);
+    // S' = scale * S for 32 columns [32*q, 32*q+32) -> smem B operand ([dk rows][dv], 2 SW128 panels)
+    auto write_sp = [&](const float (&v)[32], int q, float scale) {
+      uint8_t* dst = sp_buf + (q >> 1) * SPANEL;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         uint4 w;
@@ -434,24 +461,23 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         w.y = pack_bf16(v[8 * m + 2] * scale, v[8 * m + 3] * scale);
         w.z = pack_bf16(v[8 * m + 4] * scale, v[8 * m + 5] * scale);
         w.w = pack_bf16(v[8 * m + 6] * scale, v[8 * m + 7] * scale);
-        *reinterpret_cast<uint4*>(dst + sw128(c, 4 * hf + m)) = w;
-        if (gdst) reinterpret_cast<uint4*>(gdst)[m] = w;
+        *reinterpret_cast<uint4*>(dst + sw128(c, 4 * (q & 1) + m)) = w;
       }
     };
     {
-      const long long sidx = ((long long)(hh * nseg + s) * D + c) * D + 64 * ch;
+      const long long sidx = ((long long)(hh * nseg + s) * D + c) * D;
       const float cg = s_prev ? expf(cumG[(hh * nseg + s) * D + c]) : 0.f;
-      const float* pv = s_prev ? s_prev + ((long long)hh * D + c) * D + 64 * ch : nullptr;
+      const float* pv = s_prev ? s_prev + ((long long)hh * D + c) * D : nullptr;
       mbar_wait(&prep[0], 0);
       const float e0 = fast_exp(vr[c]);
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
-          float4 a = *reinterpret_cast<const float4*>(Sin + sidx + 32 * hf + j);
+          float4 a = *reinterpret_cast<const float4*>(Sin + sidx + 32 * q + j);
           if (pv) {
-            const float4 b = *reinterpret_cast<const float4*>(pv + 32 * hf + j);
+            const float4 b = *reinterpret_cast<const float4*>(pv + 32 * q + j);
             a.x += cg * b.x;
             a.y += cg * b.y;
             a.z += cg * b.z;
@@ -462,8 +488,8 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
           v[j + 2] = a.z;
           v[j + 3] = a.w;
         }
-        tmem_st32(s_addr + 32 * hf, v);
-        write_sp(v, hf, 0, e0);
+        tmem_st32(s_addr + 32 * q, v);
+        write_sp(v, q, e0);
       }
     }
     fence_proxy_async();
@@ -473,29 +499,32 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       const int st = n % FO_NS, ph = (n / FO_NS) & 1;
       mbar_wait(&prep[st], ph);
       const float gam_c = vgam[st * D + c], r_c = vr[st * D + c];
-      // (a) causal mask of the scores -> bf16 K-major A operand
+      // (a) causal mask of the scores -> bf16 K-major A operand (rows i = 16*qd + lane, lanes 0-15)
       mbar_wait(a_full, n & 1);
       tc_fence_after();
-      {
+      if (tid == 0) ZTRACE(tr, 5, n);
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
         float a[32];
-        tmem_ld32(taddr(tbase, 32 * qd, COL_A + 32 * ch), a);
+        tmem_ld32(taddr(tbase, 32 * qd, COL_A + 32 * hf), a);
         if (lane < 16) {
           const int i = 16 * qd + lane;
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
             uint4 w;
-            const int j0 = 32 * ch + 8 * m;
+            const int j0 = 32 * hf + 8 * m;
             w.x = pack_bf16(j0 + 0 <= i ? a[8 * m + 0] : 0.f, j0 + 1 <= i ? a[8 * m + 1] : 0.f);
             w.y = pack_bf16(j0 + 2 <= i ? a[8 * m + 2] : 0.f, j0 + 3 <= i ? a[8 * m + 3] : 0.f);
             w.z = pack_bf16(j0 + 4 <= i ? a[8 * m + 4] : 0.f, j0 + 5 <= i ? a[8 * m + 5] : 0.f);
             w.w = pack_bf16(j0 + 6 <= i ? a[8 * m + 6] : 0.f, j0 + 7 <= i ? a[8 * m + 7] : 0.f);
-            *reinterpret_cast<uint4*>(am_buf + sw128(i, 4 * ch + m)) = w;
+            *reinterpret_cast<uint4*>(am_buf + sw128(i, 4 * hf + m)) = w;
           }
         }
       }
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(a_done);
+      if (tid == 0) ZTRACE(tr, 6, n);
       // (b) state update S = e^{gam} S + e^{gam - r} (Kh^T V), and S'_{n+1} = e^{r_{n+1}} S
       const bool more = n + 1 < nt;
       float e1 = 0.f;
@@ -506,17 +535,20 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       }
       mbar_wait(kv_full, n & 1);
       tc_fence_after();
+      if (tid == 0) ZTRACE(tr, 7, n);
       {
         const float eg = fast_exp(gam_c), egr = fast_exp(gam_c - r_c);
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+          uint32_t kvr[32];
+          float sv[32];
+          tmem_ld32_nw(taddr(tbase, 32 * qd, COL_KV + 32 * q), kvr);
+          tmem_ld32_nw(s_addr + 32 * q, *reinterpret_cast<uint32_t(*)[32]>(sv));
+          tmem_wait_ld();
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          float kv[32], sv[32];
-          tmem_ld32(taddr(tbase, 32 * qd, COL_KV + 64 * ch + 32 * hf), kv);
-          tmem_ld32(s_addr + 32 * hf, sv);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) sv[j] = eg * sv[j] + egr * kv[j];
-          tmem_st32(s_addr + 32 * hf, sv);
-          if (more) write_sp(sv, hf, n + 1, e1);
+          for (int j = 0; j < 32; ++j) sv[j] = eg * sv[j] + egr * __uint_as_float(kvr[j]);
+          tmem_st32(s_addr + 32 * q, sv);
+          if (more) write_sp(sv, q, e1);
         }
       }
       tc_fence_before();
@@ -525,16 +557,19 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         fence_proxy_async();
         mbar_arrive(s_ready);
       }
-      // (c) epilogue: O tile -> global bf16
+      if (tid == 0) ZTRACE(tr, 8, n);
+      // (c) epilogue: O tile (lane half n&1) -> global bf16
       mbar_wait(o_full, n & 1);
       tc_fence_after();
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
+      if (tid == 0) ZTRACE(tr, 9, n);
+      const int ob = n & 1;
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
         float o[32];
-        tmem_ld32(taddr(tbase, 32 * qd, COL_O + 64 * ch + 32 * hf), o);
-        if (lane < 16) {
-          const int i = 16 * qd + lane;
-          uint4* dst = reinterpret_cast<uint4*>(out + ((long long)row0 + (t0 + n) * T + i) * D + 64 * ch + 32 * hf);
+        tmem_ld32(taddr(tbase, 32 * qd, COL_O + 32 * q), o);
+        if ((lane >> 4) == ob) {
+          const int i = 16 * qd + (lane & 15);
+          uint4* dst = reinterpret_cast<uint4*>(out + ((long long)row0 + (t0 + n) * T + i) * D + 32 * q);
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
             uint4 w;
@@ -547,7 +582,8 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(o_empty);
+      mbar_arrive(&o_empty[ob]);
+      if (tid == 0) ZTRACE(tr, 10, n);
     }
   }
   tc_fence_before();
@@ -601,15 +637,16 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const void* q, const void*
                     void* ws, const void* s_prev, void* o, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
-  CUtensorMap mq, mk, mv, mg;
+  CUtensorMap mq, mk, mv, mg, msp;
+  if (int rc = make_map(&msp, w.Sp, true, (unsigned long long)pl.h * pl.ntiles * D, D, 64, D, true)) return rc;
   if (int rc = map_bf16(&mq, q, pl)) return rc;
   if (int rc = map_bf16(&mk, k, pl)) return rc;
   if (int rc = map_bf16(&mv, v, pl)) return rc;
   if (int rc = map_f32(&mg, g, pl)) return rc;
   cudaFuncSetAttribute(fwd_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FO_SMEM);
-  fwd_out_kernel<<<pl.h * pl.nseg, FO_THREADS, FO_SMEM, st>>>(mq, mk, mv, mg, pl.L, pl.nseg, pl.ntiles, w.Sin,
+  fwd_out_kernel<<<pl.h * pl.nseg, FO_THREADS, FO_SMEM, st>>>(mq, mk, mv, mg, msp, (const float*)g, pl.L, pl.nseg, pl.ntiles, w.Sin,
                                                               w.cumG, (const float*)s_prev, (__nv_bfloat16*)o,
-                                                              w.Sp);
+                                                              w.Sp, g_trace_buf, g_trace_cta);
   return zgla_check_launch();
 }
 

@@ -3,6 +3,7 @@
 // up as a wrong 128x128 product instead of a wrong attention output.
 #include "tc.cuh"
 #include "zgla_internal.h"
+#include "fast_common.cuh"
 
 namespace zgla {
 
@@ -103,5 +104,71 @@ extern "C" int zgla_selftest_mma(const void* a, const void* b, float* d, int M, 
   cudaFuncSetAttribute(selftest_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   selftest_mma_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)a, (const __nv_bfloat16*)b, d, M, N, K, a_mn, b_mn, lane_off);
+  return zgla_check_launch();
+}
+
+// ---------------------------------------------------------------------------
+// Diagnostic: TMA streaming rate.  Every CTA streams `tiles_per_cta` tiles of
+// [64 rows x 128 bf16] (2 boxes of 64x64, 16 KiB) x `boxes_per_stage/2` tensors
+// through `ns` shared-memory stages; one consumer thread waits and releases.
+namespace zgla {
+__global__ void __launch_bounds__(64) selftest_stream_kernel(const __grid_constant__ CUtensorMap tm, int rows_total,
+                                                             int tiles_per_cta, int ns, int tensors, int prefetch) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int stage_bytes = tensors * 16384;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * stage_bytes);
+  uint64_t* empty = full + 8;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < ns; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int base_row = blockIdx.x * tiles_per_cta * 64;
+  if (tid == 0) {
+    for (int i = 0; i < tiles_per_cta + prefetch; ++i) {
+      if (prefetch && i < tiles_per_cta)
+        for (int t = 0; t < tensors; ++t) {
+          const int r = t * (rows_total / tensors) + base_row + i * 64;
+          tma_prefetch_2d(&tm, 0, r);
+          tma_prefetch_2d(&tm, 64, r);
+        }
+      const int j = i - prefetch;
+      if (j < 0) continue;
+      const int st = j % ns, ph = (j / ns) & 1;
+      mbar_wait(&empty[st], ph ^ 1);
+      mbar_arrive_expect_tx(&full[st], stage_bytes);
+      for (int t = 0; t < tensors; ++t) {
+        const int r = t * (rows_total / tensors) + base_row + j * 64;
+        tma_load_2d(smem + st * stage_bytes + t * 16384, &tm, &full[st], 0, r);
+        tma_load_2d(smem + st * stage_bytes + t * 16384 + 8192, &tm, &full[st], 64, r);
+      }
+    }
+  } else if (tid == 32) {
+    for (int j = 0; j < tiles_per_cta; ++j) {
+      const int st = j % ns, ph = (j / ns) & 1;
+      mbar_wait(&full[st], ph);
+      mbar_arrive(&empty[st]);
+    }
+  }
+  __syncthreads();
+}
+}  // namespace zgla
+
+extern "C" int zgla_selftest_stream(const void* src, long long rows, int tiles_per_cta, int ns, int tensors,
+                                    int prefetch, int ctas, void* stream) {
+  using namespace zgla;
+  if (ns < 1 || ns > 8 || tensors < 1) return ZGLA_ERR_CONFIG;
+  CUtensorMap m;
+  if (int rc = fast::make_map(&m, src, true, (unsigned long long)rows, 128, 64, 64, true)) return rc;
+  size_t smem = 1024 + (size_t)ns * tensors * 16384 + 256;
+  if (smem > 227 * 1024) return ZGLA_ERR_CONFIG;
+  cudaFuncSetAttribute(selftest_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  selftest_stream_kernel<<<ctas, 64, smem, (cudaStream_t)stream>>>(m, (int)rows, tiles_per_cta, ns, tensors,
+                                                                    prefetch);
   return zgla_check_launch();
 }

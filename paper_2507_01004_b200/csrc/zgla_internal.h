@@ -10,6 +10,8 @@
 namespace zgla {
 
 void set_error(const char* msg);
+extern unsigned long long* g_trace_buf;  // zgla_set_trace (diagnostics)
+extern int g_trace_cta;
 int cuda_fail(cudaError_t e, const char* where);
 
 template <typename T>

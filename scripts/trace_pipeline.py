@@ -1,0 +1,41 @@
+"""Per-tile pipeline timeline of one CTA of the fused kernels (diagnostics)."""
+import ctypes, math, sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2507_01004_b200 import ops, _native
+
+H, L, D = 16, 16384, 128
+dev = torch.device("cuda")
+gen = torch.Generator(device=dev).manual_seed(0)
+u = lambda lo, hi, dt: (torch.rand((H, L, D), device=dev, generator=gen) * (hi - lo) + lo).to(dt)
+q, k, v, do = (u(-1, 1, torch.bfloat16) for _ in range(4))
+g = u(math.log(0.9), math.log(0.999), torch.float32)
+sh = ops.ZecoShard(H, L, D, D, 64, torch.bfloat16)
+buf = torch.zeros(32 * 512, dtype=torch.int64, device=dev)
+cta = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+FWD_EV = ["tma", "prep", "mma1", "mma24", "mma3", "st_afull", "st_mask", "st_kvfull", "st_upd", "st_ofull", "st_epi", "mma_wait_s_o", "prep_start"]
+BWD_EV = ["tma", "prep", "mma_sc", "mma_wait3", "mma_grads", "st_scfull", "st_dp", "st_qdo", "st_gfull", "st_epi"]
+for it in range(3):
+    s_loc, g_tot = sh.fwd_local(k, v, g)
+    if it == 2:
+        _native.call("zgla_set_trace", ctypes.c_void_p(buf.data_ptr()), cta)
+    sh.fwd_output(q, k, v, g, None)
+    torch.cuda.synchronize()
+    if it == 2:
+        fwd_tr = buf.view(32, 512).cpu().clone(); buf.zero_()
+    d0 = sh.bwd_local(q, g, do)
+    sh.bwd_output(q, k, v, g, do, None, None)
+    torch.cuda.synchronize()
+    if it == 2:
+        bwd_tr = buf.view(32, 512).cpu().clone()
+        _native.call("zgla_set_trace", None, 0)
+
+def show(tr, names, title):
+    t0 = min(int(x) for x in tr[:len(names)].flatten() if int(x) > 0)
+    print(f"== {title}: columns are tiles, values us since first event")
+    nt = int((tr[0] > 0).sum())
+    for e, name in enumerate(names):
+        row = [(int(tr[e, n]) - t0) / 1000 if int(tr[e, n]) > 0 else float('nan') for n in range(nt)]
+        print(f"{name:14s}" + " ".join(f"{x:7.1f}" for x in row[:14]), " ... last", f"{row[-1]:.1f}")
+show(fwd_tr, FWD_EV, f"fwd_out_kernel CTA {cta}")
+show(bwd_tr, BWD_EV, f"bwd_out_kernel CTA {cta}")
