@@ -129,6 +129,7 @@ long long zgla_allscan_bytes_sent(const zgla_allscan_comm* c);
  * dev_buf (u64 [32][512]); pass NULL to disable */
 int zgla_set_trace(void* dev_buf, int cta);
 /* TMA streaming-rate probe: ctas x tiles_per_cta tiles of `tensors` x 16 KiB through ns stages */
+int zgla_selftest_tmem(int nwarps, int iters, int mode, long long* out, float* sink, void* stream);
 int zgla_selftest_stream(const void* src, long long rows, int tiles_per_cta, int ns, int tensors, int prefetch,
                          int ctas, void* stream);
 int zgla_selftest_mma(const void* a, const void* b, float* d, int M, int N, int K, int a_mn, int b_mn,

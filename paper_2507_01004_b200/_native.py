@@ -71,6 +71,7 @@ _SIGS = {
     "zgla_allscan_destroy": ([_P], _I),
     "zgla_allscan_bytes_sent": ([_P], _LL),
     "zgla_set_trace": ([_P, _I], _I),
+    "zgla_selftest_tmem": ([_I, _I, _I, _P, _P, _P], _I),
     "zgla_selftest_stream": ([_P, _LL, _I, _I, _I, _I, _I, _P], _I),
     "zgla_selftest_mma": ([_P, _P, _P, _I, _I, _I, _I, _I, _I, _P], _I),
 }

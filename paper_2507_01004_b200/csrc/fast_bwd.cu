@@ -2,13 +2,17 @@
 // bf16 q/k/v/dO/dq/dk/dv, fp32 g/dg/states, D = 128, 64-token tiles.
 //
 // One CTA per (head, segment) walks its tiles RIGHT TO LEFT carrying the fp32
-// state cotangent D (registers of 8 warps), seeded with the lifted segment-end
-// cotangent  D_end = Dend_loc + e^{G_L - G_end} ds_next  (fused bwd correction).
+// state cotangent D in TMEM, seeded with the lifted segment-end cotangent
+// D_end = Dend_loc + e^{G_L - G_end} ds_next  (fused bwd correction).  D is kept
+// in the per-tile frame Dt_n = e^{-r_n} D_n, so the recurrence
+//   Dt_n = e^{gam_n - r_n + r_{n+1}} Dt_{n+1} + Qh^T dO
+// is one per-row rescale (which also yields D' for the MMAs) followed by a
+// tcgen05 accumulation straight into TMEM (all factors <= 1).
 // The forward chunk-start states come from the forward kernel (saved as
 // S'_n = e^{r_n} S_n in bf16), so no forward recomputation walk is needed.
 // Per tile (Qh = Q e^{logb-r}, Kh = K e^{r-logb}, D' = e^{gam-r} D_{n+1}):
 //   A    = Qh Kh^T      dP = dO V^T                 (M=64, N=64)   masked in registers
-//   QDO' = Qh^T dO                                   (M=128,N=128)  D_n = e^gam D + e^r QDO'
+//   Dt  += Qh^T dO                                   (M=128,N=128)  accumulated in place
 //   dq^T = Kh^T dPm^T + S' dO^T                      (M=128,N=64)   dq = E (.) dq_raw
 //   dk^T = Qh^T dPm   + D' V^T                       (M=128,N=64)   dk = dk_raw / E
 //   dv^T = dO^T Am    + D'^T Kh^T                    (M=128,N=64)
@@ -190,13 +194,6 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         }
         mma_commit(sc_full);
         ZTRACE(tr, 2, m);
-        mbar_wait(qdo_empty, (m & 1) ^ 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < T / 16; ++kk)
-          mma_bf16_ss(tbase + BC_QDO, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(da + kk * 2048, PANEL, 1024),
-                      id_qdo, kk > 0);
-        mma_commit(qdo_full);
         mbar_wait(sc_done, m & 1);
         mbar_wait(grads_empty, (m & 1) ^ 1);
         mbar_wait(sp_full, m & 1);
@@ -211,8 +208,13 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           mma_bf16_ss(tbase + BC_DQ, sdesc(spa + (kk >> 2) * SPANEL + (kk & 3) * 32, 16, 1024),
                       sdesc(da + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024), id_kk, 1);
         mma_commit(sp_empty);
-        mbar_wait(dp_ready, m & 1);
+        mbar_wait(dp_ready, m & 1);  // D' in smem and Dt rescaled in TMEM
         tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)  // Dt += Qh^T dO
+          mma_bf16_ss(tbase + BC_QDO, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(da + kk * 2048, PANEL, 1024),
+                      id_qdo, 1);
+        mma_commit(qdo_full);
 #pragma unroll
         for (int kk = 0; kk < T / 16; ++kk) {  // dk^T = Qh^T dPm ; dv^T = dO^T Am
           mma_bf16_ss(tbase + BC_DK, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(dpma + kk * 2048, PANEL, 1024), id_mm,
@@ -290,10 +292,11 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       if (c == 0) ZTRACE(tr, 1, m);
     }
   } else {
-    // ---------------- state / epilogue warps
+    // ---------------- state / epilogue warps: thread (c, ch) owns Dt[c][64*ch .. +64] (TMEM) and,
+    //                  in the epilogue, tokens [32*ch, 32*ch+32) of channel c
     const int qd = warp & 3, ch = warp >> 2;
     const int c = 32 * qd + lane;
-    float Dst[64];
+    const uint32_t d_addr = taddr(tbase, 32 * qd, BC_QDO + 64 * ch);
     {
       const long long sidx = ((long long)(hh * nseg + s) * D + c) * D + 64 * ch;
       const float cgr = ds_next ? expf(cumGr[(hh * nseg + s) * D + c]) : 0.f;
@@ -301,30 +304,38 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const float eg = expf(gamseg[(hh * nseg + s) * D + c]);
       const long long pidx = ((long long)hh * D + c) * D + 64 * ch;
       float rho = 0.f;
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        float dv32[32];
 #pragma unroll
-      for (int j = 0; j < 64; j += 4) {
-        float4 dd = *reinterpret_cast<const float4*>(Dend + sidx + j);
-        float4 si = *reinterpret_cast<const float4*>(Sin + sidx + j);
-        const float4 ds = *reinterpret_cast<const float4*>(dS + sidx + j);
-        if (ds_next) {
-          const float4 a = *reinterpret_cast<const float4*>(ds_next + pidx + j);
-          dd.x += cgr * a.x; dd.y += cgr * a.y; dd.z += cgr * a.z; dd.w += cgr * a.w;
+        for (int j = 0; j < 32; j += 4) {
+          const int jj = 32 * hf + j;
+          float4 dd = *reinterpret_cast<const float4*>(Dend + sidx + jj);
+          float4 si = *reinterpret_cast<const float4*>(Sin + sidx + jj);
+          const float4 ds = *reinterpret_cast<const float4*>(dS + sidx + jj);
+          if (ds_next) {
+            const float4 a = *reinterpret_cast<const float4*>(ds_next + pidx + jj);
+            dd.x += cgr * a.x; dd.y += cgr * a.y; dd.z += cgr * a.z; dd.w += cgr * a.w;
+          }
+          if (s_prev) {
+            const float4 a = *reinterpret_cast<const float4*>(s_prev + pidx + jj);
+            si.x += cg * a.x; si.y += cg * a.y; si.z += cg * a.z; si.w += cg * a.w;
+          }
+          dv32[j] = dd.x; dv32[j + 1] = dd.y; dv32[j + 2] = dd.z; dv32[j + 3] = dd.w;
+          // fp32 forward state at the segment end: e^{gam_s} S_in + dS_s
+          rho += (eg * si.x + ds.x) * dd.x + (eg * si.y + ds.y) * dd.y + (eg * si.z + ds.z) * dd.z +
+                 (eg * si.w + ds.w) * dd.w;
         }
-        if (s_prev) {
-          const float4 a = *reinterpret_cast<const float4*>(s_prev + pidx + j);
-          si.x += cg * a.x; si.y += cg * a.y; si.z += cg * a.z; si.w += cg * a.w;
-        }
-        Dst[j] = dd.x; Dst[j + 1] = dd.y; Dst[j + 2] = dd.z; Dst[j + 3] = dd.w;
-        // fp32 forward state at the segment end: e^{gam_s} S_in + dS_s
-        rho += (eg * si.x + ds.x) * dd.x + (eg * si.y + ds.y) * dd.y + (eg * si.z + ds.z) * dd.z +
-               (eg * si.w + ds.w) * dd.w;
+        tmem_st32(d_addr + 32 * hf, dv32);  // Dt at the segment end (frame r = 0)
       }
       xrho[ch * D + c] = rho;
     }
+    tc_fence_before();
     named_bar(2, 256);
     if (ch == 0) xr[c] = xrho[c] + xrho[D + c];
     const uint32_t cbase = (c >> 6) * PANEL + (c & 7) * 2;
     const uint32_t cchunk = (c & 63) >> 3;
+    float r_next = 0.f;  // reference point of the previously processed (later) tile
     for (int m = 0; m < nt; ++m) {
       const int st = m % BO_NS, ph = (m / BO_NS) & 1;
       const int n = t1 - 1 - m;
@@ -354,101 +365,101 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(sc_done);
-      // (b) D' = e^{gam - r} D_{n+1} -> bf16 [c][v]
+      // (b) rescale Dt_{n+1} into this tile's frame: Dt <- f Dt, D' = f Dt (bf16 [c][v]),
+      //     f = e^{gam_n - r_n + r_{n+1}}; the MMA then accumulates Qh^T dO into Dt
       mbar_wait(&prep[st], ph);
       const float gam_c = vgam[st * D + c], r_c = vr[st * D + c];
-      {
-        const float sc = fast_exp(gam_c - r_c);
-        uint8_t* dst = dp_buf + ch * SPANEL;
-#pragma unroll
-        for (int mm = 0; mm < 8; ++mm) {
-          uint4 w;
-          w.x = pack_bf16(Dst[8 * mm] * sc, Dst[8 * mm + 1] * sc);
-          w.y = pack_bf16(Dst[8 * mm + 2] * sc, Dst[8 * mm + 3] * sc);
-          w.z = pack_bf16(Dst[8 * mm + 4] * sc, Dst[8 * mm + 5] * sc);
-          w.w = pack_bf16(Dst[8 * mm + 6] * sc, Dst[8 * mm + 7] * sc);
-          *reinterpret_cast<uint4*>(dst + sw128(c, mm)) = w;
-        }
-      }
-      fence_proxy_async();
-      mbar_arrive(dp_ready);
-      if (tid == 0) ZTRACE(tr, 6, m);
-      // (c) D_n = e^{gam} D_{n+1} + e^{r} QDO'
-      mbar_wait(qdo_full, m & 1);
+      if (m > 0) mbar_wait(qdo_full, (m - 1) & 1);
       tc_fence_after();
       {
-        const float eg = fast_exp(gam_c), er = fast_exp(r_c);
-#pragma unroll
+        const float f = fast_exp(gam_c - r_c + r_next);
+        uint8_t* dst = dp_buf + ch * SPANEL;
+#pragma unroll 1
         for (int hf = 0; hf < 2; ++hf) {
           float x[32];
-          tmem_ld32(taddr(tbase, 32 * qd, BC_QDO + 64 * ch + 32 * hf), x);
+          tmem_ld32_nw(d_addr + 32 * hf, *reinterpret_cast<uint32_t(*)[32]>(x));
+          tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) Dst[32 * hf + j] = eg * Dst[32 * hf + j] + er * x[j];
+          for (int j = 0; j < 32; ++j) x[j] *= f;
+          tmem_st32(d_addr + 32 * hf, x);
+#pragma unroll
+          for (int mm = 0; mm < 4; ++mm) {
+            uint4 w;
+            w.x = pack_bf16(x[8 * mm], x[8 * mm + 1]);
+            w.y = pack_bf16(x[8 * mm + 2], x[8 * mm + 3]);
+            w.z = pack_bf16(x[8 * mm + 4], x[8 * mm + 5]);
+            w.w = pack_bf16(x[8 * mm + 6], x[8 * mm + 7]);
+            *reinterpret_cast<uint4*>(dst + sw128(c, 4 * hf + mm)) = w;
+          }
         }
       }
+      r_next = r_c;
+      fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(qdo_empty);
-      if (tid == 0) ZTRACE(tr, 7, m);
-      // (d) epilogue: thread owns channel c, tokens [32*ch, 32*ch+32) of the tile.
-      //     pass 1: T = sum of da over my tokens (da = Qh dq_raw - Kh dk_raw needs no exponentials)
-      //     pass 2 (token order): E = e^{d}, dq/dk/dv stores, dg_i = base - prefix_{<i}(da)
+      mbar_arrive(dp_ready);
+      if (tid == 0) ZTRACE(tr, 6, m);
+      // (d) epilogue: thread owns channel c, tokens [32*ch, 32*ch+32): one TMEM pass stores dq/dk/dv and
+      //     keeps da = Qh dq_raw - Kh dk_raw; dg_i = rho_{n+1} + sum_{i' >= i in tile} da_i'
       mbar_wait(grads_full, m & 1);
       tc_fence_after();
       if (tid == 0) ZTRACE(tr, 8, m);
       const uint8_t* sb = smem + st * BO_STAGE;
       const uint32_t cols = 32 * ch;
       const uint32_t lbcol = BC_LB + 64 * (m & 1) + cols;
-      float tsum = 0.f;
-#pragma unroll 1
-      for (int q8 = 0; q8 < 4; ++q8) {
-        float gq[8], gk[8];
-        tmem_ld8(taddr(tbase, 32 * qd, BC_DQ + cols + 8 * q8), gq);
-        tmem_ld8(taddr(tbase, 32 * qd, BC_DK + cols + 8 * q8), gk);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t o = cbase + sw128(cols + 8 * q8 + u, cchunk);
-          const float qh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + o));
-          const float kh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + TILE_BF16 + o));
-          tsum += qh * gq[u] - kh * gk[u];
-        }
-      }
-      xcarry[ch * D + c] = tsum;
-      named_bar(2, 256);
-      const float rho_end = xr[c];
-      const float t_upper = xcarry[D + c], t_lower = xcarry[c];
-      // dg_i = rho_{n+1} + sum_{i' >= i in tile} da_i'
-      float base = rho_end + (ch == 0 ? t_lower + t_upper : t_upper);
       const long long tok0 = (long long)row0 + n * T + cols;
       constexpr float LOG2E = 1.4426950408889634f;
-#pragma unroll 1
-      for (int q8 = 0; q8 < 4; ++q8) {
-        float gq[8], gk[8], gv8[8], dl[8];
-        tmem_ld8(taddr(tbase, 32 * qd, BC_DQ + cols + 8 * q8), gq);
-        tmem_ld8(taddr(tbase, 32 * qd, BC_DK + cols + 8 * q8), gk);
-        tmem_ld8(taddr(tbase, 32 * qd, BC_DV + cols + 8 * q8), gv8);
-        tmem_ld8(taddr(tbase, 32 * qd, lbcol + 8 * q8), dl);
+      float da[32];
+      float tsum = 0.f;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = 8 * q8 + u;
-          const float dlt = dl[u] * LOG2E;
+      for (int h16 = 0; h16 < 2; ++h16) {
+        uint32_t gq[16], gk[16], gv16[16], dl[16];
+        tmem_ld16_nw(taddr(tbase, 32 * qd, BC_DQ + cols + 16 * h16), gq);
+        tmem_ld16_nw(taddr(tbase, 32 * qd, BC_DK + cols + 16 * h16), gk);
+        tmem_ld16_nw(taddr(tbase, 32 * qd, BC_DV + cols + 16 * h16), gv16);
+        tmem_ld16_nw(taddr(tbase, 32 * qd, lbcol + 16 * h16), dl);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int i = 16 * h16 + u;
+          const float q_raw = __uint_as_float(gq[u]), k_raw = __uint_as_float(gk[u]);
+          const float dlt = __uint_as_float(dl[u]) * LOG2E;
           const uint32_t o = cbase + sw128(cols + i, cchunk);
           const float qh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + o));
           const float kh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + TILE_BF16 + o));
-          dq[(tok0 + i) * D + c] = __float2bfloat16_rn(gq[u] * fast_exp2(dlt));
-          dk[(tok0 + i) * D + c] = __float2bfloat16_rn(gk[u] * fast_exp2(-dlt));
-          dv[(tok0 + i) * D + c] = __float2bfloat16_rn(gv8[u]);
-          dg[(tok0 + i) * D + c] = base;
-          base -= qh * gq[u] - kh * gk[u];
+#ifndef ZGLA_EXP_NOSTORE
+          dq[(tok0 + i) * D + c] = __float2bfloat16_rn(q_raw * fast_exp2(dlt));
+          dk[(tok0 + i) * D + c] = __float2bfloat16_rn(k_raw * fast_exp2(-dlt));
+          dv[(tok0 + i) * D + c] = __float2bfloat16_rn(__uint_as_float(gv16[u]));
+#else
+          if (q_raw * fast_exp2(dlt) + k_raw * fast_exp2(-dlt) + __uint_as_float(gv16[u]) == 1234.5f) dq[0] = 0;
+#endif
+          da[i] = qh * q_raw - kh * k_raw;
+          tsum += da[i];
         }
       }
       tc_fence_before();
       mbar_arrive(grads_empty);
       mbar_arrive(&lb_empty[m & 1]);
       mbar_arrive(&empty[st]);  // stage reads (Qh, Kh) done
-      named_bar(2, 256);        // everyone has read xr / xcarry of this tile
-      if (ch == 0) xr[c] = rho_end + t_lower + t_upper;  // rho at the start of this tile
+      xcarry[ch * D + c] = tsum;
+      named_bar(2, 256);
+      const float rho_end = xr[c];
+      const float t_upper = xcarry[D + c], t_lower = xcarry[c];
+      float base = rho_end + (ch == 0 ? t_lower + t_upper : t_upper);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+#ifndef ZGLA_EXP_NOSTORE
+        dg[(tok0 + i) * D + c] = base;
+#else
+        if (base == 1234.5f) dg[0] = 0;
+#endif
+        base -= da[i];
+      }
       if (tid == 0) ZTRACE(tr, 9, m);
+      named_bar(2, 256);  // everyone has read xr / xcarry of this tile
+      if (ch == 0) xr[c] = rho_end + t_lower + t_upper;  // rho at the start of this tile
     }
+    if (nt > 0) mbar_wait(qdo_full, (nt - 1) & 1);  // last Dt accumulation retired before dealloc
   }
   tc_fence_before();
   __syncthreads();

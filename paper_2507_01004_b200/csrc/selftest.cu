@@ -172,3 +172,60 @@ extern "C" int zgla_selftest_stream(const void* src, long long rows, int tiles_p
                                                                     prefetch);
   return zgla_check_launch();
 }
+
+// ---------------------------------------------------------------------------
+// Diagnostic: TMEM load/store throughput.  nwarps warps each issue `iters` x
+// tcgen05.ld.32x32b.x32 (mode 0), ld pairs before one wait (mode 1) or
+// tcgen05.st.32x32b.x32 (mode 2); clock64 delta of warp 0 is written to out[0].
+namespace zgla {
+__global__ void selftest_tmem_kernel(int iters, int mode, long long* out, float* sink) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    tmem_alloc(&slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t base = slot + ((32u * (warp & 3)) << 16) + 128u * (warp >> 2);
+  float acc = 0.f;
+  __syncthreads();
+  const long long t0 = clock64();
+  if (mode == 0) {
+    for (int i = 0; i < iters; ++i) {
+      float v[32];
+      tmem_ld32(base + 32 * (i & 3), v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc += v[j];
+    }
+  } else if (mode == 1) {
+    for (int i = 0; i < iters; i += 2) {
+      uint32_t a[32], b[32];
+      tmem_ld32_nw(base + 32 * (i & 3), a);
+      tmem_ld32_nw(base + 32 * ((i + 1) & 3), b);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc += __uint_as_float(a[j]) + __uint_as_float(b[j]);
+    }
+  } else {
+    float v[32];
+    for (int j = 0; j < 32; ++j) v[j] = (float)j;
+    for (int i = 0; i < iters; ++i) tmem_st32(base + 32 * (i & 3), v);
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) out[0] = t1 - t0;
+  if (acc == 12345.f) sink[0] = acc;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(slot, 512);
+}
+}  // namespace zgla
+
+extern "C" int zgla_selftest_tmem(int nwarps, int iters, int mode, long long* out, float* sink, void* stream) {
+  using namespace zgla;
+  if (nwarps < 1 || nwarps > 16) return ZGLA_ERR_CONFIG;
+  selftest_tmem_kernel<<<1, 32 * nwarps, 0, (cudaStream_t)stream>>>(iters, mode, out, sink);
+  return zgla_check_launch();
+}

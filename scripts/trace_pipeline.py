@@ -14,7 +14,7 @@ sh = ops.ZecoShard(H, L, D, D, 64, torch.bfloat16)
 buf = torch.zeros(32 * 512, dtype=torch.int64, device=dev)
 cta = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 FWD_EV = ["tma", "prep", "mma1", "mma24", "mma3", "st_afull", "st_mask", "st_kvfull", "st_upd", "st_ofull", "st_epi", "mma_wait_s_o", "prep_start"]
-BWD_EV = ["tma", "prep", "mma_sc", "mma_wait3", "mma_grads", "st_scfull", "st_dp", "st_qdo", "st_gfull", "st_epi"]
+BWD_EV = ["tma", "prep", "mma_sc", "mma_wait3", "mma_grads", "st_scfull", "st_dp", "unused", "st_gfull", "st_epi"]
 for it in range(3):
     s_loc, g_tot = sh.fwd_local(k, v, g)
     if it == 2:
