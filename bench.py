@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     return p.parse_args()
 
 
@@ -274,21 +275,42 @@ def main():
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
+    # per-phase breakdown: eager launches with events between phases (diagnostic only)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(min(args.steps, 20))]
+    for e in evs:
+        step(e)
+    torch.cuda.synchronize()
+    per_phase = {p: statistics.mean(e[j].elapsed_time(e[j + 1]) for e in evs) for j, p in enumerate(phases)}
+    # the timed region: the step captured once as a CUDA graph (N=1; with peers the All-Scan
+    # kernels carry host-side epochs, so N>1 replays eager launches) and replayed K times
+    use_graph = world == 1 and not args.no_graph
+    graph = None
+    if use_graph:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step()
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        for _ in range(3):
+            graph.replay()
+    run_step = graph.replay if graph is not None else step
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
-        start.record(stream)
+        start.record()
         for i in range(args.steps):
-            step(evs[i])
-        end.record(stream)
+            run_step()
+        end.record()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end)
-    per_phase = {p: statistics.mean(e[j].elapsed_time(e[j + 1]) for e in evs) for j, p in enumerate(phases)}
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -361,6 +383,7 @@ def main():
                    "l2": "inputs 384 MiB per GPU > 126 MiB L2 (no flush needed)"},
         "per_gpu_tokens_per_s": L / (ms_step / 1e3),
         "phase_ms": {p: round(per_phase[p], 5) for p in phases},
+        "timed_as": "cuda_graph" if graph is not None else "eager",
         "roofline": {"kernel": {"fwd_output": "fwd_out_kernel", "bwd_output": "bwd_out_kernel",
                                 "fwd_local": "seg_state_kernel<0>+fwd_scan", "bwd_local": "seg_state_kernel<1>+bwd_scan"}[dom],
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

@@ -48,6 +48,19 @@ struct Link {
   T* scanned_out;
 };
 
+template <typename T>
+struct V4 {
+  T x, y, z, w;
+};
+__device__ __forceinline__ V4<float> ldcg4(const V4<float>* p) {
+  const float4 v = __ldcg(reinterpret_cast<const float4*>(p));
+  return {v.x, v.y, v.z, v.w};
+}
+__device__ __forceinline__ V4<double> ldcg4(const V4<double>* p) {
+  const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+  return {a.x, a.y, b.x, b.y};
+}
 __device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ float scan_update(float gl, float r, float x) {
@@ -66,29 +79,64 @@ __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+template <bool SYS>
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  if (SYS) asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+template <bool SYS>
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  if (SYS) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ void fence_acq_rel() {
+  if (SYS) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+// poll with relaxed loads; one acquire fence once the value is seen (bar.sync then publishes it to the CTA)
+template <bool SYS>
 __device__ __forceinline__ bool spin_until_geq(const unsigned* p, unsigned target) {
   long long t0 = clock64();
-  while ((int)(ld_acquire_sys(p) - target) < 0) {
+  while ((int)(ld_relaxed<SYS>(p) - target) < 0) {
     if (clock64() - t0 > (1ll << 34)) return false;  // ~8 s at 2 GHz: treat as deadlock
   }
+  fence_acq_rel<SYS>();
   return true;
 }
 
 // one CTA's share of the chain for one rank
-template <typename T>
+template <typename T, bool SYS>
 __device__ void rank_body(const Link<T>& L, int h, int dk, int dv, int K, int cta, int nctas, unsigned epoch,
                           int* err) {
   const int rows = dk / K;
   const int blk_el = rows * dv;          // elements of one head inside one pipeline block
-  const int per_cta = (blk_el + nctas - 1) / nctas;
-  const int lo = cta * per_cta, hi = min(blk_el, lo + per_cta);
+  const bool vec4 = (dv % 4) == 0;
+  int per_cta = (blk_el + nctas - 1) / nctas;
+  if (vec4) per_cta = (per_cta + 3) & ~3;
+  const int lo = min(blk_el, cta * per_cta), hi = min(blk_el, lo + per_cta);
   __shared__ int ok;
+  // back-pressure: my slice of the successor's inbox may only be overwritten once the successor has
+  // consumed it in the previous epoch (one ACK per CTA slice, independent of the block count K)
+  if (threadIdx.x == 0 && L.succ_inbox && !spin_until_geq<SYS>(L.my_ack + cta, epoch - 1)) {
+    atomicExch(err, 1);
+    printf("zgla all-scan: ack wait timed out (deadlock)\n");
+    __trap();
+  }
   for (int b = 0; b < K; ++b) {
     const int fidx = b * nctas + cta;
     if (threadIdx.x == 0) {
       bool good = true;
-      if (L.inbox) good = spin_until_geq(L.flags + fidx, epoch);
-      if (good && L.succ_inbox) good = spin_until_geq(L.my_ack + fidx, epoch - 1);
+      if (L.inbox) good = spin_until_geq<SYS>(L.flags + fidx, epoch);
       ok = good;
       if (!good) {
         atomicExch(err, 1);
@@ -98,26 +146,60 @@ __device__ void rank_body(const Link<T>& L, int h, int dk, int dv, int K, int ct
     }
     __syncthreads();
     if (!ok) return;
-    for (int hh = 0; hh < h; ++hh) {
-      const long long base = (long long)hh * dk * dv + (long long)b * blk_el;
-      for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const long long e = base + i;
-        const int c = b * rows + i / dv;
-        const T r = L.inbox ? ldcg(L.inbox + e) : T(0);
-        // same rounding sequence as the reference update (gate * recv, then + local)
-        const T s = scan_update(L.logdecay[hh * dk + c], r, L.local[e]);
-        if (L.recv_out) L.recv_out[e] = r;
-        L.scanned_out[e] = s;
-        if (L.succ_inbox) L.succ_inbox[e] = s;
+    if (vec4) {
+      // float4 path: all loads of a batch are issued before any use (latency-bound otherwise)
+      const int lo4 = lo >> 2, n4 = (hi - lo) >> 2, blk4 = blk_el >> 2;
+      const int total = h * n4;
+      for (int u0 = threadIdx.x; u0 < total; u0 += 4 * blockDim.x) {
+        V4<T> r[4], x[4];
+        T gl[4];
+        long long e4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int u = u0 + k * blockDim.x;
+          const int hh = u / max(n4, 1), i4 = lo4 + u % max(n4, 1);
+          e4[k] = ((long long)hh * dk * dv + (long long)b * blk_el) / 4 + i4;
+          if (u < total) {
+            const int c = b * rows + (i4 * 4) / dv;
+            gl[k] = L.logdecay[hh * dk + c];
+            x[k] = reinterpret_cast<const V4<T>*>(L.local)[e4[k]];
+            r[k] = L.inbox ? ldcg4(reinterpret_cast<const V4<T>*>(L.inbox) + e4[k]) : V4<T>{0, 0, 0, 0};
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (u0 + k * blockDim.x >= total) break;
+          V4<T> sc;
+          sc.x = scan_update(gl[k], r[k].x, x[k].x);
+          sc.y = scan_update(gl[k], r[k].y, x[k].y);
+          sc.z = scan_update(gl[k], r[k].z, x[k].z);
+          sc.w = scan_update(gl[k], r[k].w, x[k].w);
+          if (L.recv_out) reinterpret_cast<V4<T>*>(L.recv_out)[e4[k]] = r[k];
+          reinterpret_cast<V4<T>*>(L.scanned_out)[e4[k]] = sc;
+          if (L.succ_inbox) reinterpret_cast<V4<T>*>(L.succ_inbox)[e4[k]] = sc;
+        }
+      }
+      (void)blk4;
+    } else {
+      for (int hh = 0; hh < h; ++hh) {
+        const long long base = (long long)hh * dk * dv + (long long)b * blk_el;
+        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+          const long long e = base + i;
+          const int c = b * rows + i / dv;
+          const T r = L.inbox ? ldcg(L.inbox + e) : T(0);
+          // same rounding sequence as the reference update (gate * recv, then + local)
+          const T s = scan_update(L.logdecay[hh * dk + c], r, L.local[e]);
+          if (L.recv_out) L.recv_out[e] = r;
+          L.scanned_out[e] = s;
+          if (L.succ_inbox) L.succ_inbox[e] = s;
+        }
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      if (L.succ_inbox) st_release_sys(L.succ_flags + fidx, epoch);
-      if (L.ack_to_pred) st_release_sys(L.ack_to_pred + fidx, epoch);
-    }
+    // release at system scope is cumulative over the CTA's stores observed through bar.sync
+    if (threadIdx.x == 0 && L.succ_inbox) st_release<SYS>(L.succ_flags + fidx, epoch);
   }
+  if (threadIdx.x == 0 && L.ack_to_pred) st_release<SYS>(L.ack_to_pred + cta, epoch);
 }
 
 // list form: P ranks on one device, recv[p] doubles as rank p's inbox
@@ -145,13 +227,13 @@ __global__ void __launch_bounds__(kThreads) local_chain_kernel(int P, int h, int
     // no ACK protocol needed: flags are cleared before every list-form call
     L.my_ack = flags + (long long)P * fl;  // all-zero dummy; epoch-1 == 0 passes
   }
-  rank_body(L, h, dk, dv, K, cta, kCtasPerRank, 1u, err);
+  rank_body<T, false>(L, h, dk, dv, K, cta, kCtasPerRank, 1u, err);  // one device: gpu scope
 }
 
 // SPMD form: one rank per process
 __global__ void __launch_bounds__(kThreads) rank_chain_kernel(Link<float> L, int h, int dk, int dv, int K, unsigned epoch,
                                                               int* err) {
-  rank_body(L, h, dk, dv, K, blockIdx.x, gridDim.x, epoch, err);
+  rank_body<float, true>(L, h, dk, dv, K, blockIdx.x, gridDim.x, epoch, err);  // peers: system scope
 }
 
 __global__ void copy_kernel(long long n, const float* src, float* dst) {

@@ -483,7 +483,7 @@ int fast_bwd_output(const zgla_shape* s, int num_sms, const void* q, const void*
   if (int rc = make_map(&mdo, d_out, true, rows, D, 64, T, true)) return rc;
   if (int rc = make_map(&msp, w.Sp, true, (unsigned long long)pl.h * pl.ntiles * D, D, 64, D, true)) return rc;
   if (int rc = make_map(&mg, g, false, rows, D, D, T, false)) return rc;
-  cudaFuncSetAttribute(bwd_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BO_SMEM);
+  set_smem_once((const void*)bwd_out_kernel, (int)BO_SMEM);
   bwd_out_kernel<<<pl.h * pl.nseg, BO_THREADS, BO_SMEM, st>>>(
       mq, mk, mv, mdo, msp, mg, (const float*)g, pl.L, pl.nseg, pl.ntiles, w.Sin, w.cumG, w.dS, w.gam,
       (const float*)s_prev, w.Dend, w.cumGr, (const float*)ds_next, (__nv_bfloat16*)dq, (__nv_bfloat16*)dk,

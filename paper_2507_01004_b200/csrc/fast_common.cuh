@@ -136,6 +136,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if ((buf) != nullptr && (n) < TRACE_TILES) (buf)[(ev) * TRACE_TILES + (n)] = gtimer(); \
   } while (0)
 
+// opt a kernel into large dynamic shared memory once per process (the attribute is sticky)
+inline void set_smem_once(const void* fn, int bytes) {
+  static const void* done[16] = {nullptr};
+  for (auto& d : done) {
+    if (d == fn) return;
+    if (d == nullptr) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      d = fn;
+      return;
+    }
+  }
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
 // ---- device helpers
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

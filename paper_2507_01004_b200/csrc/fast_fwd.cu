@@ -617,7 +617,7 @@ int launch_seg_state(int dir, const Plan& pl, const void* a, const void* b, cons
   if (int rc = map_bf16(&mb, b, pl)) return rc;
   if (int rc = map_f32(&mg, g, pl)) return rc;
   auto kern = dir == 0 ? seg_state_kernel<0> : seg_state_kernel<1>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KS_SMEM);
+  set_smem_once((const void*)kern, (int)KS_SMEM);
   kern<<<pl.h * pl.nseg, KS_THREADS, KS_SMEM, st>>>(ma, mb, mg, pl.L, pl.nseg, pl.ntiles, out_state, out_gam);
   return zgla_check_launch();
 }
@@ -643,7 +643,7 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const void* q, const void*
   if (int rc = map_bf16(&mk, k, pl)) return rc;
   if (int rc = map_bf16(&mv, v, pl)) return rc;
   if (int rc = map_f32(&mg, g, pl)) return rc;
-  cudaFuncSetAttribute(fwd_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FO_SMEM);
+  set_smem_once((const void*)fwd_out_kernel, (int)FO_SMEM);
   fwd_out_kernel<<<pl.h * pl.nseg, FO_THREADS, FO_SMEM, st>>>(mq, mk, mv, mg, msp, (const float*)g, pl.L, pl.nseg, pl.ntiles, w.Sin,
                                                               w.cumG, (const float*)s_prev, (__nv_bfloat16*)o,
                                                               w.Sp, g_trace_buf, g_trace_cta);
