@@ -411,30 +411,36 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       float da[32];
       float tsum = 0.f;
 #pragma unroll
-      for (int h16 = 0; h16 < 2; ++h16) {
-        uint32_t gq[16], gk[16], gv16[16], dl[16];
-        tmem_ld16_nw(taddr(tbase, 32 * qd, BC_DQ + cols + 16 * h16), gq);
-        tmem_ld16_nw(taddr(tbase, 32 * qd, BC_DK + cols + 16 * h16), gk);
-        tmem_ld16_nw(taddr(tbase, 32 * qd, BC_DV + cols + 16 * h16), gv16);
-        tmem_ld16_nw(taddr(tbase, 32 * qd, lbcol + 16 * h16), dl);
+      for (int h8 = 0; h8 < 4; ++h8) {
+        uint32_t gq[8], gk[8], gv8[8], dl[8];
+        tmem_ld8_nw(taddr(tbase, 32 * qd, BC_DQ + cols + 8 * h8), gq);
+        tmem_ld8_nw(taddr(tbase, 32 * qd, BC_DK + cols + 8 * h8), gk);
+        tmem_ld8_nw(taddr(tbase, 32 * qd, BC_DV + cols + 8 * h8), gv8);
+        tmem_ld8_nw(taddr(tbase, 32 * qd, lbcol + 8 * h8), dl);
+        // shared-memory operands first: the global stores below go through generic pointers and
+        // would otherwise serialise every later shared load behind them
+        float qh[8], kh[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t o = cbase + sw128(cols + 8 * h8 + u, cchunk);
+          qh[u] = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + o));
+          kh[u] = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + TILE_BF16 + o));
+        }
         tmem_wait_ld();
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int i = 16 * h16 + u;
+        for (int u = 0; u < 8; ++u) {
+          const int i = 8 * h8 + u;
           const float q_raw = __uint_as_float(gq[u]), k_raw = __uint_as_float(gk[u]);
           const float dlt = __uint_as_float(dl[u]) * LOG2E;
-          const uint32_t o = cbase + sw128(cols + i, cchunk);
-          const float qh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + o));
-          const float kh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sb + TILE_BF16 + o));
+          da[i] = qh[u] * q_raw - kh[u] * k_raw;
+          tsum += da[i];
 #ifndef ZGLA_EXP_NOSTORE
           dq[(tok0 + i) * D + c] = __float2bfloat16_rn(q_raw * fast_exp2(dlt));
           dk[(tok0 + i) * D + c] = __float2bfloat16_rn(k_raw * fast_exp2(-dlt));
-          dv[(tok0 + i) * D + c] = __float2bfloat16_rn(__uint_as_float(gv16[u]));
+          dv[(tok0 + i) * D + c] = __float2bfloat16_rn(__uint_as_float(gv8[u]));
 #else
-          if (q_raw * fast_exp2(dlt) + k_raw * fast_exp2(-dlt) + __uint_as_float(gv16[u]) == 1234.5f) dq[0] = 0;
+          if (q_raw * fast_exp2(dlt) + k_raw * fast_exp2(-dlt) + __uint_as_float(gv8[u]) == 1234.5f) dq[0] = 0;
 #endif
-          da[i] = qh * q_raw - kh * k_raw;
-          tsum += da[i];
         }
       }
       tc_fence_before();
