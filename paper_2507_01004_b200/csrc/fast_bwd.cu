@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
                    __nv_bfloat16* __restrict__ dv, float* __restrict__ dg, unsigned long long* trace,
                    int trace_cta) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sp_buf = smem + BO_OFF_SP;
   uint8_t* dp_buf = smem + BO_OFF_DP;
   uint8_t* am_buf = smem + BO_OFF_AM;

@@ -34,7 +34,8 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
                      const __grid_constant__ CUtensorMap tm_g, long long L, int nseg, int ntiles,
                      float* __restrict__ out_state, float* __restrict__ out_gam) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + KS_OFF_BAR);
   uint64_t* full = bars;
   uint64_t* empty = bars + KS_NS;
@@ -251,7 +252,8 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
                    const float* __restrict__ s_prev, __nv_bfloat16* __restrict__ out,
                    __nv_bfloat16* __restrict__ sp_save, unsigned long long* trace, int trace_cta) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sp_buf = smem + FO_OFF_SP;
   uint8_t* am_buf = smem + FO_OFF_AM;
   float* vgam = reinterpret_cast<float*>(smem + FO_OFF_VEC);  // [NS][D]

@@ -15,7 +15,8 @@ __global__ void __launch_bounds__(128) selftest_mma_kernel(const __nv_bfloat16* 
                                                            float* __restrict__ d_out, int M, int N, int K,
                                                            int a_mn, int b_mn, int lane_off) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x;
@@ -115,7 +116,8 @@ namespace zgla {
 __global__ void __launch_bounds__(64) selftest_stream_kernel(const __grid_constant__ CUtensorMap tm, int rows_total,
                                                              int tiles_per_cta, int ns, int tensors, int prefetch) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stage_bytes = tensors * 16384;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * stage_bytes);
   uint64_t* empty = full + 8;
