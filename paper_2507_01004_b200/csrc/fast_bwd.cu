@@ -255,7 +255,9 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const float rr = lb[31];
 #pragma unroll
       for (int r = 0; r < 64; ++r) lb[r] -= rr;
+      if (c == 0) ZTRACE(tr, 10, m);
       mbar_wait(&full[st], ph);
+      if (c == 0) ZTRACE(tr, 11, m);
       vgam[st * D + c] = lb[63] + rr;
       vr[st * D + c] = rr;
 #pragma unroll
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
     const int c = 32 * qd + lane;
     const uint32_t d_addr = taddr(tbase, 32 * qd, BC_QDO + 64 * ch);
     {
-      const long long sidx = ((long long)(hh * nseg + s) * D + c) * D + 64 * ch;
+      const long long sidx = (long long)(hh * nseg + s) * D * D + c;  // column-major workspace states
       const float cgr = ds_next ? expf(cumGr[(hh * nseg + s) * D + c]) : 0.f;
       const float cg = s_prev ? expf(cumG[(hh * nseg + s) * D + c]) : 0.f;
       const float eg = expf(gamseg[(hh * nseg + s) * D + c]);
@@ -311,9 +313,10 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
           const int jj = 32 * hf + j;
-          float4 dd = *reinterpret_cast<const float4*>(Dend + sidx + jj);
-          float4 si = *reinterpret_cast<const float4*>(Sin + sidx + jj);
-          const float4 ds = *reinterpret_cast<const float4*>(dS + sidx + jj);
+          const long long o = sidx + (long long)(64 * ch + jj) * D;
+          float4 dd = make_float4(Dend[o], Dend[o + D], Dend[o + 2 * D], Dend[o + 3 * D]);
+          float4 si = make_float4(Sin[o], Sin[o + D], Sin[o + 2 * D], Sin[o + 3 * D]);
+          const float4 ds = make_float4(dS[o], dS[o + D], dS[o + 2 * D], dS[o + 3 * D]);
           if (ds_next) {
             const float4 a = *reinterpret_cast<const float4*>(ds_next + pidx + jj);
             dd.x += cgr * a.x; dd.y += cgr * a.y; dd.z += cgr * a.z; dd.w += cgr * a.w;
@@ -333,6 +336,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
     }
     tc_fence_before();
     named_bar(2, 256);
+    if (tid == 0) ZTRACE(tr, 7, 0);
     if (ch == 0) xr[c] = xrho[c] + xrho[D + c];
     const uint32_t cbase = (c >> 6) * PANEL + (c & 7) * 2;
     const uint32_t cchunk = (c & 63) >> 3;

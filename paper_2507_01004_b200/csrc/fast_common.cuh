@@ -37,6 +37,8 @@ __host__ __device__ inline void seg_range(int s, int nseg, int ntiles, int& t0, 
 }
 
 // workspace carve-up (fp32 unless noted), per shard
+// Segment states are stored column-major per (head, segment): element (c, v) at v * D + c, so the
+// thread-per-channel (TMEM lane) readers and writers touch 128 contiguous bytes per warp.
 struct Ws {
   float* dS;      // [h][nseg][D][D]  fwd: segment-local final state from zero
   float* gam;     // [h][nseg][D]     segment total log decay

@@ -167,14 +167,14 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
     if (grp == 0) {
       mbar_wait(done, 0);
       tc_fence_after();
-      float* dst = out_state + ((long long)(hh * nseg + s) * D + c) * D;
+      // workspace states are column-major ([v][c]) so lanes (= channels c) store contiguously
+      float* dst = out_state + (long long)(hh * nseg + s) * D * D + c;
 #pragma unroll
       for (int chn = 0; chn < D / 32; ++chn) {
         float v[32];
         tmem_ld32(taddr(tbase, warp * 32, chn * 32), v);
 #pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          *reinterpret_cast<float4*>(dst + chn * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        for (int j = 0; j < 32; ++j) dst[(chn * 32 + j) * D] = v[j];
       }
     }
     if (nt > 0 && grp == ((nt - 1) & 1)) out_gam[(long long)(hh * nseg + s) * D + c] = last_tot;
@@ -191,15 +191,15 @@ __global__ void fwd_scan_kernel(int h, int nseg, const float* __restrict__ dS, c
                                 float* __restrict__ g_tot) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)h * D * D) return;
-  const int hh = (int)(idx / (D * D)), e = (int)(idx % (D * D)), c = e / D;
+  const int hh = (int)(idx / (D * D)), e = (int)(idx % (D * D)), c = e % D, vv = e / D;
   float run = 0.f;
   for (int s = 0; s < nseg; ++s) {
     const long long o = ((long long)(hh * nseg + s)) * D * D + e;
     Sin[o] = run;
     run = expf(gam[(hh * nseg + s) * D + c]) * run + dS[o];
   }
-  if (s_local) s_local[idx] = run;
-  if ((e % D) == 0) {
+  if (s_local) s_local[((long long)hh * D + c) * D + vv] = run;  // API layout: row-major [h][c][v]
+  if (vv == 0) {
     float cm = 0.f;
     for (int s = 0; s < nseg; ++s) {
       cumG[(hh * nseg + s) * D + c] = cm;
@@ -214,15 +214,15 @@ __global__ void bwd_scan_kernel(int h, int nseg, const float* __restrict__ dD, c
                                 float* __restrict__ Dend, float* __restrict__ cumGr, float* __restrict__ ds0) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)h * D * D) return;
-  const int hh = (int)(idx / (D * D)), e = (int)(idx % (D * D)), c = e / D;
+  const int hh = (int)(idx / (D * D)), e = (int)(idx % (D * D)), c = e % D, vv = e / D;
   float run = 0.f;
   for (int s = nseg - 1; s >= 0; --s) {
     const long long o = ((long long)(hh * nseg + s)) * D * D + e;
     Dend[o] = run;
     run = expf(gam[(hh * nseg + s) * D + c]) * run + dD[o];
   }
-  if (ds0) ds0[idx] = run;
-  if ((e % D) == 0) {
+  if (ds0) ds0[((long long)hh * D + c) * D + vv] = run;
+  if (vv == 0) {
     float cm = 0.f;
     for (int s = nseg - 1; s >= 0; --s) {
       cumGr[(hh * nseg + s) * D + c] = cm;
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       }
     };
     {
-      const long long sidx = ((long long)(hh * nseg + s) * D + c) * D;
+      const long long sidx = (long long)(hh * nseg + s) * D * D + c;  // column-major workspace state
       const float cg = s_prev ? expf(cumG[(hh * nseg + s) * D + c]) : 0.f;
       const float* pv = s_prev ? s_prev + ((long long)hh * D + c) * D : nullptr;
       mbar_wait(&prep[0], 0);
@@ -477,7 +477,9 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
-          float4 a = *reinterpret_cast<const float4*>(Sin + sidx + 32 * q + j);
+          const int col = 32 * q + j;
+          float4 a = make_float4(Sin[sidx + col * D], Sin[sidx + (col + 1) * D], Sin[sidx + (col + 2) * D],
+                                 Sin[sidx + (col + 3) * D]);
           if (pv) {
             const float4 b = *reinterpret_cast<const float4*>(pv + 32 * q + j);
             a.x += cg * b.x;

@@ -14,7 +14,7 @@ sh = ops.ZecoShard(H, L, D, D, 64, torch.bfloat16)
 buf = torch.zeros(32 * 512, dtype=torch.int64, device=dev)
 cta = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 FWD_EV = ["tma", "prep", "mma1", "mma24", "mma3", "st_afull", "st_mask", "st_kvfull", "st_upd", "st_ofull", "st_epi", "mma_wait_s_o", "prep_start"]
-BWD_EV = ["tma", "prep", "mma_sc", "mma_wait3", "mma_grads", "st_scfull", "st_dp", "unused", "st_gfull", "st_epi"]
+BWD_EV = ["tma", "prep", "mma_sc", "mma_wait3", "mma_grads", "st_scfull", "st_dp", "st_prologue", "st_gfull", "st_epi", "prep_g", "prep_full"]
 for it in range(3):
     s_loc, g_tot = sh.fwd_local(k, v, g)
     if it == 2:
@@ -39,3 +39,18 @@ def show(tr, names, title):
         print(f"{name:14s}" + " ".join(f"{x:7.1f}" for x in row[:14]), " ... last", f"{row[-1]:.1f}")
 show(fwd_tr, FWD_EV, f"fwd_out_kernel CTA {cta}")
 show(bwd_tr, BWD_EV, f"bwd_out_kernel CTA {cta}")
+
+def steady(tr, names, pairs, title):
+    """mean durations (us) over the steady tiles 2..nt-2 for (name, from_event, to_event) pairs"""
+    nt = int((tr[0] > 0).sum())
+    ix = {n: i for i, n in enumerate(names)}
+    out = []
+    period = (int(tr[ix[pairs[0][2]], nt - 2]) - int(tr[ix[pairs[0][2]], 2])) / (nt - 4) / 1000
+    for name, a, b in pairs:
+        d = [(int(tr[ix[b], n]) - int(tr[ix[a], n])) / 1000 for n in range(2, nt - 1)]
+        out.append(f"{name}={sum(d) / len(d):.2f}")
+    print(f"STEADY {title}: period={period:.2f}us " + " ".join(out))
+
+steady(bwd_tr, BWD_EV, [("epi", "st_gfull", "st_epi"), ("mma", "st_dp", "st_gfull"),
+                        ("mask_dp", "st_scfull", "st_dp"), ("tma2prep", "tma", "prep")], "bwd")
+steady(fwd_tr, FWD_EV, [("epi", "st_ofull", "st_epi"), ("tma2prep", "tma", "prep")], "fwd")
