@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--e2e-groups", type=int, default=8, help="head groups of the host-buffer pipeline")
     p.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     return p.parse_args()
 
@@ -321,28 +322,12 @@ def main():
     # ---- end to end through the C-ABI with pinned HOST buffers (copies inside the timed region)
     host_in = [x.cpu().pin_memory() for x in (q, k, v, g, do)]
     host_out = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (o,) + grads]
-    dev_in = [torch.empty_like(x) for x in (q, k, v, g, do)]
     h2d = sum(x.numel() * x.element_size() for x in host_in)
     d2h = sum(x.numel() * x.element_size() for x in host_out)
 
     def e2e_step():
-        for hsrc, dd in zip(host_in, dev_in):
-            dd.copy_(hsrc, non_blocking=True)
-        qq, kk, vv, gg, dd_o = dev_in
-        s_loc, g_tot = layer.shard.fwd_local(kk, vv, gg)
-        prev = None
-        if comm is not None:
-            recv, _ = comm(s_loc, g_tot, args.blocks, 0)
-            prev = recv if rank > 0 else None
-        layer.shard.fwd_output(qq, kk, vv, gg, prev, out=o)
-        ds0 = layer.shard.bwd_local(qq, gg, dd_o)
-        ds_next = None
-        if comm is not None:
-            rb, _ = comm(ds0, g_tot, args.blocks, 1)
-            ds_next = rb if rank < world - 1 else None
-        layer.shard.bwd_output(qq, kk, vv, gg, dd_o, prev, ds_next, grads=grads)
-        for hdst, src in zip(host_out, (o,) + grads):
-            hdst.copy_(src, non_blocking=True)
+        # the public host-buffer call: heads pipelined H2D -> kernels -> D2H on three streams
+        layer.forward_backward_host(host_in, host_out, head_groups=args.e2e_groups)
 
     e2e_step()
     torch.cuda.synchronize()
@@ -395,7 +380,9 @@ def main():
                           "tflops": step_flops / (ms_step / 1e3) / 1e12,
                           "tensor_frac": step_flops / (ms_step / 1e3) / 1e12 / tc_peak},
         "e2e": {"value": world * L / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "call": f"ZecoRank.forward_backward_host -> zgla_zeco_fwd_bwd_host, pinned host buffers, "
+                        f"{args.e2e_groups} head groups pipelined H2D/kernels/D2H"},
         "gpu_launches": args.steps * (6 + (4 if world > 1 else 0)),
         "clocks": clk.summary(),
     }

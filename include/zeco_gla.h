@@ -123,6 +123,22 @@ int zgla_allscan_run(zgla_allscan_comm* c, int num_blocks, int direction, const 
                      const float* log_decay, float* recv, float* scanned, void* stream);
 int zgla_allscan_destroy(zgla_allscan_comm* c);
 long long zgla_allscan_bytes_sent(const zgla_allscan_comm* c);
+/* rank, world size and head count the communicator was created with (any pointer may be NULL) */
+int zgla_allscan_info(const zgla_allscan_comm* c, int* rank, int* world, int* heads);
+
+/* ---- host-buffer layer call (the reference's verify/bench flow, glasp/cli.py:241-361) ----
+ * One ZeCO GLA layer forward + backward with q,k,v,g,dO and o,dq,dk,dv,dg in HOST memory
+ * (pinned for full PCIe speed; layouts and dtypes as above).  Heads are cut into head_groups
+ * groups pipelined over three streams (H2D / kernels / D2H), so transfers in both directions
+ * overlap each other and the kernels.  comm may be NULL (one rank); otherwise it must have been
+ * created for heads / head_groups heads and every rank runs the groups in the same order.
+ * dev_buf: device scratch of zgla_zeco_fwd_bwd_host_bytes() bytes.  Stream-ordered: the host
+ * outputs are complete when `stream` has drained. */
+long long zgla_zeco_fwd_bwd_host_bytes(const zgla_shape* s, int num_sms, int head_groups);
+int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head_groups, zgla_allscan_comm* comm,
+                           int num_blocks, const void* q, const void* k, const void* v, const void* g,
+                           const void* d_out, void* o, void* dq, void* dk, void* dv, void* dg, void* dev_buf,
+                           long long dev_buf_bytes, void* stream);
 
 /* ---- diagnostics -------------------------------------------------------- */
 /* record per-tile pipeline timestamps (%globaltimer) of CTA `cta` of the fused kernels into

@@ -70,6 +70,9 @@ _SIGS = {
     "zgla_allscan_run": ([_P, _I, _I, _P, _P, _P, _P, _P], _I),
     "zgla_allscan_destroy": ([_P], _I),
     "zgla_allscan_bytes_sent": ([_P], _LL),
+    "zgla_allscan_info": ([_P, _P, _P, _P], _I),
+    "zgla_zeco_fwd_bwd_host_bytes": ([ctypes.POINTER(Shape), _I, _I], _LL),
+    "zgla_zeco_fwd_bwd_host": ([ctypes.POINTER(Shape), _I, _I, _P, _I] + [_P] * 11 + [_LL, _P], _I),
     "zgla_set_trace": ([_P, _I], _I),
     "zgla_selftest_tmem": ([_I, _I, _I, _P, _P, _P], _I),
     "zgla_selftest_stream": ([_P, _LL, _I, _I, _I, _I, _I, _P], _I),

@@ -236,11 +236,6 @@ __global__ void __launch_bounds__(kThreads) rank_chain_kernel(Link<float> L, int
   rank_body<float, true>(L, h, dk, dv, K, blockIdx.x, gridDim.x, epoch, err);  // peers: system scope
 }
 
-__global__ void copy_kernel(long long n, const float* src, float* dst) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = __ldcg(src + i);
-}
-
 // list-form workspace (flags + error word), grown on demand
 struct Scratch {
   std::mutex mu;
@@ -412,19 +407,23 @@ extern "C" int zgla_allscan_run(zgla_allscan_comm* c, int num_blocks, int direct
   L.succ_inbox = is_sink ? nullptr : inbox_of(c, succ, d);
   L.succ_flags = is_sink ? nullptr : flags_of(c, succ, d);
   L.my_ack = ack_of(c, c->region, d);
-  L.recv_out = nullptr;
+  // recv is written by the chain kernel itself (zeros at the source), before the inbox is acked: a
+  // predecessor running ahead into the next epoch can never overwrite data not yet copied out
+  L.recv_out = recv;
   L.scanned_out = scanned;
   if (c->world == 1) L.inbox = nullptr;
   rank_chain_kernel<<<kCtasPerRank, kThreads, 0, st>>>(L, c->h, c->dk, c->dv, num_blocks, epoch, c->err);
   if (int rc = zgla_check_launch()) return rc;
-  if (recv) {
-    if (L.inbox)
-      copy_kernel<<<(unsigned)((c->nel + 255) / 256), 256, 0, st>>>(c->nel, L.inbox, recv);
-    else
-      cudaMemsetAsync(recv, 0, c->nel * sizeof(float), st);
-  }
   if (!is_sink) c->bytes_sent += c->nel * (long long)sizeof(float);
   return zgla_check_launch();
+}
+
+extern "C" int zgla_allscan_info(const zgla_allscan_comm* c, int* rank, int* world, int* heads) {
+  if (!c) return ZGLA_ERR_DIMS;
+  if (rank) *rank = c->rank;
+  if (world) *world = c->world;
+  if (heads) *heads = c->h;
+  return ZGLA_OK;
 }
 
 extern "C" long long zgla_allscan_bytes_sent(const zgla_allscan_comm* c) { return c ? c->bytes_sent : -1; }

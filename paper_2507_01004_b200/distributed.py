@@ -141,6 +141,45 @@ class ZecoRank:
         self._prev, self._g_tot = prev, g_tot
         return self.shard.fwd_output(q, k, v, g, prev, out=out)
 
+    def forward_backward_host(self, host_in, host_out, head_groups=16):
+        """One layer forward + backward with inputs (q, k, v, g, dO) and outputs (o, dq, dk, dv, dg) in
+        HOST memory (CPU torch tensors, pinned for full PCIe rate), through the C-ABI call
+        ``zgla_zeco_fwd_bwd_host``: heads are pipelined in ``head_groups`` groups so host->device,
+        kernels and device->host overlap.  Stream-ordered on the current stream."""
+        geo = self.shard.geo
+        names = ("q", "k", "v", "g", "d_out", "o", "dq", "dk", "dv", "dg")
+        acc = geo.acc
+        dts = (geo.dtype, geo.dtype, geo.dtype, acc, geo.dtype, geo.dtype, geo.dtype, geo.dtype, geo.dtype, acc)
+        widths = (geo.dk, geo.dk, geo.dv, geo.dk, geo.dv, geo.dv, geo.dk, geo.dk, geo.dv, geo.dk)
+        ts = tuple(host_in) + tuple(host_out)
+        if len(ts) != 10:
+            raise ConfigError("forward_backward_host expects 5 inputs (q, k, v, g, dO) and 5 outputs")
+        for t, n, dt, w in zip(ts, names, dts, widths):
+            if not isinstance(t, torch.Tensor) or t.is_cuda or not t.is_contiguous():
+                raise ConfigError(f"{n} must be a contiguous host (CPU) tensor")
+            if t.dtype != dt or tuple(t.shape) != (geo.h, geo.L, w):
+                raise ConfigError(f"{n}: expected {dt} {(geo.h, geo.L, w)}, got {t.dtype} {tuple(t.shape)}")
+        if not 1 <= head_groups <= geo.h or (self.world > 1 and geo.h % head_groups):
+            raise ConfigError(f"head_groups {head_groups} must be in [1, {geo.h}] (and divide the heads with peers)")
+        lib = _native.load()
+        nbytes = lib.zgla_zeco_fwd_bwd_host_bytes(ctypes.byref(self.shard.shape), self.shard.sms, head_groups)
+        if nbytes < 0:
+            raise ConfigError("invalid host-call geometry")
+        buf = getattr(self, "_host_buf", None)
+        if buf is None or buf.numel() < nbytes:
+            buf = self._host_buf = torch.empty(nbytes, dtype=torch.uint8, device=self.shard.device)
+        comm = None
+        if self.world > 1:
+            cache = self.__dict__.setdefault("_host_comm", {})
+            if head_groups not in cache:
+                cache[head_groups] = AllScanP2P(geo.h // head_groups, geo.dk, geo.dv, group=self.comm.group)
+            comm = cache[head_groups]._h
+        _native.call("zgla_zeco_fwd_bwd_host", ctypes.byref(self.shard.shape), self.shard.sms, head_groups, comm,
+                     self.K, *(ctypes.c_void_p(t.data_ptr()) for t in ts), ops._p(buf), buf.numel(), ops._stream())
+        if self.world > 1:
+            self.ledger[("all_scan", "sent")] += geo.h * geo.dk * geo.dv * (
+                (self.rank < self.world - 1) + (self.rank > 0))
+
     def backward(self, q, k, v, g, d_out, grads=None):
         ds0 = self.shard.bwd_local(q, g, d_out)
         ds_next = None

@@ -1,0 +1,89 @@
+"""The host-buffer layer call (zgla_zeco_fwd_bwd_host, via ZecoRank.forward_backward_host):
+head groups pipelined H2D -> kernels -> D2H must give the device path's results.
+
+* head_groups = 1 runs exactly the device path's plan: bitwise equal;
+* head_groups > 1 re-plans the segments per group (different fp32 summation order): checked
+  against the CPU oracle at the north-star tolerance (bf16 rtol 1e-2, fp32 mode 1e-4)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import gla_oracle as orc
+from tests.helpers import TOL_BF16, TOL_F32, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(h, L, D, dtype, seed=3):
+    q, k, v, g = orc.make_inputs(1, L, h, D, D, seed, orc.LONG_DECAY_LOW, orc.LONG_DECAY_HIGH)
+    do = orc.make_cotangent(seed, h, L, D)
+    acc = torch.float32
+    host = [torch.from_numpy(np.ascontiguousarray(x)).to(dt).pin_memory()
+            for x, dt in ((q, dtype), (k, dtype), (v, dtype), (g, acc), (do, dtype))]
+    return host
+
+
+def _outs(h, L, D, dtype):
+    return [torch.empty((h, L, D), dtype=dt).pin_memory() for dt in (dtype, dtype, dtype, dtype, torch.float32)]
+
+
+def _device_path(host, h, L, D, dtype):
+    from paper_2507_01004_b200 import distributed as zd
+    layer = zd.ZecoRank(h, L, D, 64, dtype)
+    q, k, v, g, do = (x.cuda() for x in host)
+    o = layer.forward(q, k, v, g)
+    grads = layer.backward(q, k, v, g, do)
+    torch.cuda.synchronize()
+    return [o.cpu()] + [x.cpu() for x in grads]
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_host_call_one_group_bitwise(dtype):
+    from paper_2507_01004_b200 import distributed as zd
+    h, L, D = 4, 512, 128
+    host = _case(h, L, D, dtype)
+    want = _device_path(host, h, L, D, dtype)
+    layer = zd.ZecoRank(h, L, D, 64, dtype)
+    out = _outs(h, L, D, dtype)
+    layer.forward_backward_host(host, out, head_groups=1)
+    torch.cuda.current_stream().synchronize()
+    for name, a, b in zip(("o", "dq", "dk", "dv", "dg"), out, want):
+        assert torch.equal(a, b), name
+
+
+@pytest.mark.parametrize("dtype,groups,h", [(torch.bfloat16, 2, 4), (torch.bfloat16, 4, 4), (torch.float32, 4, 4),
+                                           (torch.bfloat16, 3, 6), (torch.bfloat16, 4, 7)])
+def test_host_call_groups_vs_oracle(dtype, groups, h):
+    """groups of 1 head at both ends (tapered split) when heads > groups, uniform otherwise"""
+    from paper_2507_01004_b200 import distributed as zd
+    L, D = 512, 128
+    host = _case(h, L, D, dtype)
+    layer = zd.ZecoRank(h, L, D, 64, dtype)
+    out = _outs(h, L, D, dtype)
+    # run twice: the second call reuses streams, events and the device buffer
+    for _ in range(2):
+        for t in out:
+            t.zero_()
+        layer.forward_backward_host(host, out, head_groups=groups)
+        torch.cuda.current_stream().synchronize()
+    q, k, v, g, do = (x.double().numpy() for x in host)
+    want_o, saved, _ = orc.zeco_forward(q, k, v, g, 1, 64)
+    want_g, _ = orc.zeco_backward(q, k, v, g, do, 1, 64, saved)
+    tol = TOL_BF16 if dtype == torch.bfloat16 else TOL_F32
+    for name, a, b in zip(("o", "dq", "dk", "dv", "dg"), out, [want_o] + list(want_g)):
+        err = rel(a.double().numpy(), b)
+        assert err <= tol, f"{name}: rel err {err:.3e} > {tol}"
+
+
+def test_host_call_rejects_bad_args():
+    from paper_2507_01004_b200 import distributed as zd
+    from paper_2507_01004_b200.errors import ConfigError
+    h, L, D = 4, 256, 128
+    host = _case(h, L, D, torch.bfloat16)
+    layer = zd.ZecoRank(h, L, D, 64, torch.bfloat16)
+    out = _outs(h, L, D, torch.bfloat16)
+    with pytest.raises(ConfigError):
+        layer.forward_backward_host(host, out, head_groups=5)
+    with pytest.raises(ConfigError):
+        layer.forward_backward_host([x.cuda() for x in host], out, head_groups=1)
