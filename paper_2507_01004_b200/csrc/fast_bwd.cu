@@ -121,6 +121,8 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 12) {
     // ---------------- TMA producer (tiles right to left)
@@ -495,10 +497,12 @@ int fast_bwd_output(const zgla_shape* s, int num_sms, const void* q, const void*
   if (int rc = make_map(&msp, w.Sp, true, (unsigned long long)pl.h * pl.ntiles * D, D, 64, D, true)) return rc;
   if (int rc = make_map(&mg, g, false, rows, D, D, T, false)) return rc;
   set_smem_once((const void*)bwd_out_kernel, (int)BO_SMEM);
-  bwd_out_kernel<<<pl.h * pl.nseg, BO_THREADS, BO_SMEM, st>>>(
-      mq, mk, mv, mdo, msp, mg, (const float*)g, pl.L, pl.nseg, pl.ntiles, w.Sin, w.cumG, w.dS, w.gam,
-      (const float*)s_prev, w.Dend, w.cumGr, (const float*)ds_next, (__nv_bfloat16*)dq, (__nv_bfloat16*)dk,
-      (__nv_bfloat16*)dv, (float*)dg, g_trace_buf, g_trace_cta);
+  if (cudaError_t e = launch_k(bwd_out_kernel, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp, mg,
+                                (const float*)g, pl.L, pl.nseg, pl.ntiles, (const float*)w.Sin, (const float*)w.cumG,
+                                (const float*)w.dS, (const float*)w.gam, (const float*)s_prev, (const float*)w.Dend,
+                                (const float*)w.cumGr, (const float*)ds_next, (__nv_bfloat16*)dq,
+                                (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, (float*)dg, g_trace_buf, g_trace_cta))
+    return cuda_fail(e, "bwd_out_kernel");
   return zgla_check_launch();
 }
 

@@ -70,6 +70,8 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 8) {
     if (lane == 0) {
@@ -189,6 +191,8 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
 __global__ void fwd_scan_kernel(int h, int nseg, const float* __restrict__ dS, const float* __restrict__ gam,
                                 float* __restrict__ Sin, float* __restrict__ cumG, float* __restrict__ s_local,
                                 float* __restrict__ g_tot) {
+  pdl_wait();
+  pdl_trigger();
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)h * D * D) return;
   const int hh = (int)(idx / (D * D)), e = (int)(idx % (D * D)), c = e % D, vv = e / D;
@@ -212,6 +216,8 @@ __global__ void fwd_scan_kernel(int h, int nseg, const float* __restrict__ dS, c
 // backward: Dend[s] = sum_{s'>s} e^{gam(s+1..s'-1)} dD[s'];  ds_local0 = Dend[-1] inclusive of all; cumGr
 __global__ void bwd_scan_kernel(int h, int nseg, const float* __restrict__ dD, const float* __restrict__ gam,
                                 float* __restrict__ Dend, float* __restrict__ cumGr, float* __restrict__ ds0) {
+  pdl_wait();
+  pdl_trigger();
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)h * D * D) return;
   const int hh = (int)(idx / (D * D)), e = (int)(idx % (D * D)), c = e % D, vv = e / D;
@@ -305,6 +311,8 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 12) {
     // ---------------- TMA producer
@@ -622,7 +630,9 @@ int launch_seg_state(int dir, const Plan& pl, const void* a, const void* b, cons
   if (int rc = map_f32(&mg, g, pl)) return rc;
   auto kern = dir == 0 ? seg_state_kernel<0> : seg_state_kernel<1>;
   set_smem_once((const void*)kern, (int)KS_SMEM);
-  kern<<<pl.h * pl.nseg, KS_THREADS, KS_SMEM, st>>>(ma, mb, mg, pl.L, pl.nseg, pl.ntiles, out_state, out_gam);
+  if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, KS_THREADS, KS_SMEM, st, ma, mb, mg, pl.L, pl.nseg,
+                                pl.ntiles, out_state, out_gam))
+    return cuda_fail(e, "seg_state_kernel");
   return zgla_check_launch();
 }
 
@@ -632,8 +642,9 @@ int fast_fwd_local(const zgla_shape* s, int num_sms, const void* k, const void* 
   Ws w = carve(pl, ws);
   if (int rc = launch_seg_state(0, pl, k, v, g, w.dS, w.gam, st)) return rc;
   const long long n = (long long)pl.h * D * D;
-  fwd_scan_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl.h, pl.nseg, w.dS, w.gam, w.Sin, w.cumG,
-                                                              (float*)s_local, (float*)g_tot);
+  if (cudaError_t e = launch_k(fwd_scan_kernel, (unsigned)((n + 255) / 256), 256, 0, st, pl.h, pl.nseg,
+                                (const float*)w.dS, (const float*)w.gam, w.Sin, w.cumG, (float*)s_local, (float*)g_tot))
+    return cuda_fail(e, "fwd_scan_kernel");
   return zgla_check_launch();
 }
 
@@ -648,9 +659,10 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const void* q, const void*
   if (int rc = map_bf16(&mv, v, pl)) return rc;
   if (int rc = map_f32(&mg, g, pl)) return rc;
   set_smem_once((const void*)fwd_out_kernel, (int)FO_SMEM);
-  fwd_out_kernel<<<pl.h * pl.nseg, FO_THREADS, FO_SMEM, st>>>(mq, mk, mv, mg, msp, (const float*)g, pl.L, pl.nseg, pl.ntiles, w.Sin,
-                                                              w.cumG, (const float*)s_prev, (__nv_bfloat16*)o,
-                                                              w.Sp, g_trace_buf, g_trace_cta);
+  if (cudaError_t e = launch_k(fwd_out_kernel, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
+                                (const float*)g, pl.L, pl.nseg, pl.ntiles, (const float*)w.Sin, (const float*)w.cumG,
+                                (const float*)s_prev, (__nv_bfloat16*)o, w.Sp, g_trace_buf, g_trace_cta))
+    return cuda_fail(e, "fwd_out_kernel");
   return zgla_check_launch();
 }
 
@@ -660,8 +672,9 @@ int fast_bwd_local(const zgla_shape* s, int num_sms, const void* q, const void* 
   Ws w = carve(pl, ws);
   if (int rc = launch_seg_state(1, pl, q, d_out, g, w.dD, w.gam, st)) return rc;
   const long long n = (long long)pl.h * D * D;
-  bwd_scan_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl.h, pl.nseg, w.dD, w.gam, w.Dend, w.cumGr,
-                                                              (float*)ds0);
+  if (cudaError_t e = launch_k(bwd_scan_kernel, (unsigned)((n + 255) / 256), 256, 0, st, pl.h, pl.nseg,
+                                (const float*)w.dD, (const float*)w.gam, w.Dend, w.cumGr, (float*)ds0))
+    return cuda_fail(e, "bwd_scan_kernel");
   return zgla_check_launch();
 }
 
