@@ -90,7 +90,8 @@ def load(path: str | None = None):
     global _lib
     with _lock:
         if _lib is None:
-            p = path or LIB_PATH
+            # ZGLA_LIB: alternative build of the same library (compile-variant A/B experiments)
+            p = path or os.environ.get("ZGLA_LIB") or LIB_PATH
             if not os.path.exists(p):
                 raise errors.NativeLibraryError(
                     f"{p} is missing: build it with `make` or `python -c 'import __graft_entry__ as g; g.build()'`"

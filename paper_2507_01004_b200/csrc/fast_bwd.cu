@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   const int nt = t1 - t0;
   const int row0 = (int)(hh * L);
   unsigned long long* tr = (trace != nullptr && (int)blockIdx.x == trace_cta) ? trace : nullptr;
+  if (trace != nullptr && threadIdx.x == 0) cta_trace_begin(trace);
 
   if (tid == 0) {
     for (int i = 0; i < BO_NS; ++i) {
@@ -211,20 +212,15 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           mma_bf16_ss(tbase + BC_DQ, sdesc(spa + (kk >> 2) * SPANEL + (kk & 3) * 32, 16, 1024),
                       sdesc(da + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024), id_kk, 1);
         mma_commit(sp_empty);
-        mbar_wait(dp_ready, m & 1);  // D' in smem and Dt rescaled in TMEM
-        tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < T / 16; ++kk)  // Dt += Qh^T dO
-          mma_bf16_ss(tbase + BC_QDO, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(da + kk * 2048, PANEL, 1024),
-                      id_qdo, 1);
-        mma_commit(qdo_full);
-#pragma unroll
-        for (int kk = 0; kk < T / 16; ++kk) {  // dk^T = Qh^T dPm ; dv^T = dO^T Am
+        for (int kk = 0; kk < T / 16; ++kk) {  // dk^T = Qh^T dPm ; dv^T = dO^T Am  (independent of D')
           mma_bf16_ss(tbase + BC_DK, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(dpma + kk * 2048, PANEL, 1024), id_mm,
                       kk > 0);
           mma_bf16_ss(tbase + BC_DV, sdesc(da + kk * 2048, PANEL, 1024), sdesc(ama + kk * 2048, PANEL, 1024), id_mm,
                       kk > 0);
         }
+        mbar_wait(dp_ready, m & 1);  // D' in smem and Dt rescaled in TMEM
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {  // dk^T += D' V^T ; dv^T += D'^T Kh^T
           const uint32_t boff = (kk >> 2) * PANEL + (kk & 3) * 32;
@@ -233,6 +229,12 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           mma_bf16_ss(tbase + BC_DV, sdesc(dpa + kk * 2048, SPANEL, 1024), sdesc(ka + boff, 16, 1024), id_mk, 1);
         }
         mma_commit(grads_full);
+        // the state cotangent update is needed only by the next tile's rescale: issue it last
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)  // Dt += Qh^T dO
+          mma_bf16_ss(tbase + BC_QDO, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(da + kk * 2048, PANEL, 1024),
+                      id_qdo, 1);
+        mma_commit(qdo_full);
         ZTRACE(tr, 4, m);
       }
     }
@@ -476,6 +478,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (trace != nullptr && threadIdx.x == 0) cta_trace_end(trace);
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
 

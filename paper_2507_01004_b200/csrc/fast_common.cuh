@@ -141,6 +141,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if ((buf) != nullptr && (n) < TRACE_TILES) (buf)[(ev) * TRACE_TILES + (n)] = gtimer(); \
   } while (0)
 
+// per-CTA lifetime (diagnostics): rows 26/27/28 of the trace buffer hold start, end and SM id by CTA
+__device__ __forceinline__ void cta_trace_begin(unsigned long long* buf) {
+  if (blockIdx.x < TRACE_TILES) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    buf[26 * TRACE_TILES + blockIdx.x] = gtimer();
+    buf[28 * TRACE_TILES + blockIdx.x] = smid;
+  }
+}
+__device__ __forceinline__ void cta_trace_end(unsigned long long* buf) {
+  if (blockIdx.x < TRACE_TILES) buf[27 * TRACE_TILES + blockIdx.x] = gtimer();
+}
+
 // opt a kernel into large dynamic shared memory once per process (the attribute is sticky)
 inline void set_smem_once(const void* fn, int bytes) {
   static const void* done[16] = {nullptr};

@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   const int nt = t1 - t0;
   const int row0 = (int)(hh * L);
   unsigned long long* tr = (trace != nullptr && (int)blockIdx.x == trace_cta) ? trace : nullptr;
+  if (trace != nullptr && threadIdx.x == 0) cta_trace_begin(trace);
 
   if (tid == 0) {
     for (int i = 0; i < FO_NS; ++i) {
@@ -600,6 +601,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (trace != nullptr && threadIdx.x == 0) cta_trace_end(trace);
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
 

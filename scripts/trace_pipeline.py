@@ -54,3 +54,19 @@ def steady(tr, names, pairs, title):
 steady(bwd_tr, BWD_EV, [("epi", "st_gfull", "st_epi"), ("mma", "st_dp", "st_gfull"),
                         ("mask_dp", "st_scfull", "st_dp"), ("tma2prep", "tma", "prep")], "bwd")
 steady(fwd_tr, FWD_EV, [("epi", "st_ofull", "st_epi"), ("tma2prep", "tma", "prep")], "fwd")
+
+
+def ctas(tr, title):
+    """per-CTA lifetimes (us): spread of start and end across the grid"""
+    st, en = tr[26].numpy().astype("int64"), tr[27].numpy().astype("int64")
+    n = int((st > 0).sum())
+    st, en = st[:n], en[:n]
+    t0 = st.min()
+    dur = (en - st) / 1000
+    print(f"CTAS {title}: n={n} start spread {(st.max() - t0) / 1000:.1f}us, end first {(en.min() - t0) / 1000:.1f} "
+          f"last {(en.max() - t0) / 1000:.1f}us; duration min {dur.min():.1f} median {sorted(dur)[n // 2]:.1f} max {dur.max():.1f}")
+    slow = sorted(range(n), key=lambda i: -dur[i])[:6]
+    print("   slowest:", [(i, round(float(dur[i]), 1), int(tr[28, i])) for i in slow])
+
+ctas(fwd_tr, "fwd_out")
+ctas(bwd_tr, "bwd_out")
