@@ -51,6 +51,52 @@ static int get_ctx(Ctx** out, size_t nev) {
   return ZGLA_OK;
 }
 
+// SM-driven transfers between device memory and pinned (device-mapped) host memory, kept as an
+// option (ZGLA_XFER=sm: both directions, ZGLA_XFER=hyb: SM reads for H2D + DMA for D2H).  Measured
+// on the B200 box (cfg2, 402 MB each way): bidirectional copy-engine DMA loses ~50 us per extra
+// copy pair once transfers are split (1 copy 8.1 ms, 40 copies 10.3 ms, 80 copies 11.2 ms); SM
+// reads of pinned host memory reach ~98 GB/s alone but drop to 25-35 GB/s as soon as any D2H
+// traffic runs concurrently, so whole-call times were 12.7-15 ms against 10.2-10.5 ms with DMA.
+// The default is therefore DMA.
+struct Xfer {
+  const uint4* src[5];
+  uint4* dst[5];
+  long long n16[5];  // 16-byte units per tensor
+  int count;
+};
+// Each direction gets XFER_CTAS whole SMs (1024 threads x 4 x 16 B = 64 KB in flight per SM); the
+// group kernels are planned for the remaining num_sms - 2 * XFER_CTAS SMs, so transfers never wait
+// for a compute wave and vice versa.
+constexpr int XFER_CTAS = 8, XFER_THREADS = 1024, XFER_UNROLL = 4;
+
+__global__ void __launch_bounds__(XFER_THREADS, 1) xfer_kernel(Xfer x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (int t = 0; t < x.count; ++t) {
+    const uint4* __restrict__ src = x.src[t];
+    uint4* __restrict__ dst = x.dst[t];
+    const long long n = x.n16[t];
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (XFER_UNROLL - 1) * stride < n; i += XFER_UNROLL * stride) {
+      uint4 v[XFER_UNROLL];
+#pragma unroll
+      for (int u = 0; u < XFER_UNROLL; ++u) v[u] = __ldcs(src + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < XFER_UNROLL; ++u) __stcs(dst + i + u * stride, v[u]);
+    }
+    for (; i < n; i += stride) __stcs(dst + i, __ldcs(src + i));
+  }
+}
+
+// host pointer usable by device code (pinned + mapped under UVA)?
+static bool device_mapped(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer == p;
+}
+
 inline long long al256(long long x) { return (x + 255) & ~255ll; }
 inline int esize(int dt) { return dt == ZGLA_BF16 ? 2 : dt == ZGLA_F32 ? 4 : 8; }
 inline int asize(int dt) { return dt == ZGLA_F64 ? 8 : 4; }
@@ -161,6 +207,16 @@ extern "C" int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head
   const void* hin[5] = {q, k, v, g, d_out};
   void* hout[5] = {o, dq, dk, dv, dg};
   cudaEvent_t ev_start = cx->ev[2 * G], ev_done = cx->ev[2 * G + 1];
+  // optional SM-driven transfers (every host buffer device-mapped and 16-byte aligned)
+  static const int xmode = [] {  // 0 dma, 1 sm both directions, 2 sm h2d + dma d2h
+    const char* e = std::getenv("ZGLA_XFER");
+    return !e ? 0 : e[0] == 's' ? 1 : e[0] == 'h' ? 2 : 0;
+  }();
+  bool sm_xfer = xmode != 0;
+  for (int i = 0; i < 5 && sm_xfer; ++i)
+    sm_xfer = device_mapped(hin[i]) && device_mapped(hout[i]) &&
+              ((reinterpret_cast<uintptr_t>(hin[i]) | reinterpret_cast<uintptr_t>(hout[i])) & 15) == 0 &&
+              ph_in[i] % 16 == 0 && ph_out[i] % 16 == 0;
   // diagnostics: ZGLA_HOST_TRACE=1 prints the per-group timeline (synchronises; never in timed runs)
   static const bool trace = std::getenv("ZGLA_HOST_TRACE") != nullptr;
   std::vector<cudaEvent_t> tev;
@@ -173,14 +229,26 @@ extern "C" int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head
   if (cudaError_t r = cudaEventRecord(ev_start, st)) return cuda_fail(r, "zgla_zeco_fwd_bwd_host");
   cudaStreamWaitEvent(cx->h2d, ev_start, 0);
   cudaStreamWaitEvent(cx->d2h, ev_start, 0);
+  const int csms = sm_xfer && num_sms > 4 * XFER_CTAS ? num_sms - (xmode == 1 ? 2 : 1) * XFER_CTAS : num_sms;
   for (int j = 0; j < G; ++j) {
     const int h0 = gb[j], h1 = gb[j + 1];
     const int hg = h1 - h0;
-    for (int i = 0; i < 5; ++i) {
-      if (cudaError_t r = cudaMemcpyAsync(base + lo.in[i] + h0 * ph_in[i],
-                                          reinterpret_cast<const unsigned char*>(hin[i]) + h0 * ph_in[i],
-                                          hg * ph_in[i], cudaMemcpyHostToDevice, cx->h2d))
-        return cuda_fail(r, "zgla_zeco_fwd_bwd_host h2d");
+    if (sm_xfer) {
+      Xfer x;
+      x.count = 5;
+      for (int i = 0; i < 5; ++i) {
+        x.src[i] = reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(hin[i]) + h0 * ph_in[i]);
+        x.dst[i] = reinterpret_cast<uint4*>(base + lo.in[i] + h0 * ph_in[i]);
+        x.n16[i] = hg * ph_in[i] / 16;
+      }
+      xfer_kernel<<<XFER_CTAS, XFER_THREADS, 0, cx->h2d>>>(x);
+    } else {
+      for (int i = 0; i < 5; ++i) {
+        if (cudaError_t r = cudaMemcpyAsync(base + lo.in[i] + h0 * ph_in[i],
+                                            reinterpret_cast<const unsigned char*>(hin[i]) + h0 * ph_in[i],
+                                            hg * ph_in[i], cudaMemcpyHostToDevice, cx->h2d))
+          return cuda_fail(r, "zgla_zeco_fwd_bwd_host h2d");
+      }
     }
     cudaEventRecord(cx->ev[2 * j], cx->h2d);
     if (trace) cudaEventRecord(tev[3 * j], cx->h2d);
@@ -199,30 +267,41 @@ extern "C" int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head
     float* ds0 = reinterpret_cast<float*>(base + lo.st[4]);
     float* recv_b = reinterpret_cast<float*>(base + lo.st[5]);
     float* scan_b = reinterpret_cast<float*>(base + lo.st[6]);
-    if (int rc = zgla_zeco_fwd_local(&gs, num_sms, in[1], in[2], in[3], ws, s_local, g_tot, st)) return rc;
+    if (int rc = zgla_zeco_fwd_local(&gs, csms, in[1], in[2], in[3], ws, s_local, g_tot, st)) return rc;
     const void* prev = nullptr;
     if (peers) {
       if (int rc = zgla_allscan_run(comm, num_blocks, ZGLA_FWD, s_local, g_tot, recv_f, scan_f, st)) return rc;
       prev = rank > 0 ? recv_f : nullptr;
     }
-    if (int rc = zgla_zeco_fwd_output(&gs, num_sms, in[0], in[1], in[2], in[3], ws, prev, out[0], st)) return rc;
-    if (int rc = zgla_zeco_bwd_local(&gs, num_sms, in[0], in[3], in[4], ws, ds0, st)) return rc;
+    if (int rc = zgla_zeco_fwd_output(&gs, csms, in[0], in[1], in[2], in[3], ws, prev, out[0], st)) return rc;
+    if (int rc = zgla_zeco_bwd_local(&gs, csms, in[0], in[3], in[4], ws, ds0, st)) return rc;
     const void* ds_next = nullptr;
     if (peers) {
       if (int rc = zgla_allscan_run(comm, num_blocks, ZGLA_BWD, ds0, g_tot, recv_b, scan_b, st)) return rc;
       ds_next = rank < world - 1 ? recv_b : nullptr;
     }
-    if (int rc = zgla_zeco_bwd_output(&gs, num_sms, in[0], in[1], in[2], in[3], in[4], ws, prev, ds_next, out[1],
+    if (int rc = zgla_zeco_bwd_output(&gs, csms, in[0], in[1], in[2], in[3], in[4], ws, prev, ds_next, out[1],
                                       out[2], out[3], out[4], st))
       return rc;
     cudaEventRecord(cx->ev[2 * j + 1], st);
     if (trace) cudaEventRecord(tev[3 * j + 1], st);
     cudaStreamWaitEvent(cx->d2h, cx->ev[2 * j + 1], 0);
-    for (int i = 0; i < 5; ++i) {
-      if (cudaError_t r = cudaMemcpyAsync(reinterpret_cast<unsigned char*>(hout[i]) + h0 * ph_out[i],
-                                          base + lo.out[i] + h0 * ph_out[i], hg * ph_out[i],
-                                          cudaMemcpyDeviceToHost, cx->d2h))
-        return cuda_fail(r, "zgla_zeco_fwd_bwd_host d2h");
+    if (sm_xfer && xmode == 1) {
+      Xfer x;
+      x.count = 5;
+      for (int i = 0; i < 5; ++i) {
+        x.src[i] = reinterpret_cast<const uint4*>(base + lo.out[i] + h0 * ph_out[i]);
+        x.dst[i] = reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(hout[i]) + h0 * ph_out[i]);
+        x.n16[i] = hg * ph_out[i] / 16;
+      }
+      xfer_kernel<<<XFER_CTAS, XFER_THREADS, 0, cx->d2h>>>(x);
+    } else {
+      for (int i = 0; i < 5; ++i) {
+        if (cudaError_t r = cudaMemcpyAsync(reinterpret_cast<unsigned char*>(hout[i]) + h0 * ph_out[i],
+                                            base + lo.out[i] + h0 * ph_out[i], hg * ph_out[i],
+                                            cudaMemcpyDeviceToHost, cx->d2h))
+          return cuda_fail(r, "zgla_zeco_fwd_bwd_host d2h");
+      }
     }
     if (trace) cudaEventRecord(tev[3 * j + 2], cx->d2h);
   }
