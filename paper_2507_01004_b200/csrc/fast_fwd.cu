@@ -188,6 +188,11 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
 
 // ============================================================== K2 / K5
 // forward: Sin[s] = sum_{s'<s} e^{gam(s'+1..s-1)} dS[s'];  S_local = inclusive;  cumG / G_tot
+// One thread per state element walks the segments in order; the loads of a batch of SCAN_B segments
+// are issued before the dependent multiply-adds, so the walk costs ~nseg/SCAN_B memory latencies
+// instead of nseg.
+constexpr int SCAN_B = 8;
+
 __global__ void fwd_scan_kernel(int h, int nseg, const float* __restrict__ dS, const float* __restrict__ gam,
                                 float* __restrict__ Sin, float* __restrict__ cumG, float* __restrict__ s_local,
                                 float* __restrict__ g_tot) {
@@ -196,21 +201,29 @@ __global__ void fwd_scan_kernel(int h, int nseg, const float* __restrict__ dS, c
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)h * D * D) return;
   const int hh = (int)(idx / (D * D)), e = (int)(idx % (D * D)), c = e % D, vv = e / D;
-  float run = 0.f;
-  for (int s = 0; s < nseg; ++s) {
-    const long long o = ((long long)(hh * nseg + s)) * D * D + e;
-    Sin[o] = run;
-    run = expf(gam[(hh * nseg + s) * D + c]) * run + dS[o];
+  const long long base = (long long)hh * nseg * D * D + e;
+  const float* gm = gam + (long long)hh * nseg * D + c;
+  float run = 0.f, cm = 0.f;
+  for (int s0 = 0; s0 < nseg; s0 += SCAN_B) {
+    float x[SCAN_B], gg[SCAN_B];
+#pragma unroll
+    for (int j = 0; j < SCAN_B; ++j) {
+      const bool ok = s0 + j < nseg;
+      x[j] = ok ? __ldcs(dS + base + (long long)(s0 + j) * D * D) : 0.f;
+      gg[j] = ok ? __ldg(gm + (s0 + j) * D) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < SCAN_B; ++j) {
+      if (s0 + j < nseg) {
+        Sin[base + (long long)(s0 + j) * D * D] = run;
+        run = expf(gg[j]) * run + x[j];
+        if (vv == 0) cumG[(long long)(hh * nseg + s0 + j) * D + c] = cm;
+        cm += gg[j];
+      }
+    }
   }
   if (s_local) s_local[((long long)hh * D + c) * D + vv] = run;  // API layout: row-major [h][c][v]
-  if (vv == 0) {
-    float cm = 0.f;
-    for (int s = 0; s < nseg; ++s) {
-      cumG[(hh * nseg + s) * D + c] = cm;
-      cm += gam[(hh * nseg + s) * D + c];
-    }
-    if (g_tot) g_tot[hh * D + c] = cm;
-  }
+  if (vv == 0 && g_tot) g_tot[hh * D + c] = cm;
 }
 
 // backward: Dend[s] = sum_{s'>s} e^{gam(s+1..s'-1)} dD[s'];  ds_local0 = Dend[-1] inclusive of all; cumGr
@@ -221,20 +234,28 @@ __global__ void bwd_scan_kernel(int h, int nseg, const float* __restrict__ dD, c
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)h * D * D) return;
   const int hh = (int)(idx / (D * D)), e = (int)(idx % (D * D)), c = e % D, vv = e / D;
-  float run = 0.f;
-  for (int s = nseg - 1; s >= 0; --s) {
-    const long long o = ((long long)(hh * nseg + s)) * D * D + e;
-    Dend[o] = run;
-    run = expf(gam[(hh * nseg + s) * D + c]) * run + dD[o];
-  }
-  if (ds0) ds0[((long long)hh * D + c) * D + vv] = run;
-  if (vv == 0) {
-    float cm = 0.f;
-    for (int s = nseg - 1; s >= 0; --s) {
-      cumGr[(hh * nseg + s) * D + c] = cm;
-      cm += gam[(hh * nseg + s) * D + c];
+  const long long base = (long long)hh * nseg * D * D + e;
+  const float* gm = gam + (long long)hh * nseg * D + c;
+  float run = 0.f, cm = 0.f;
+  for (int s0 = nseg - 1; s0 >= 0; s0 -= SCAN_B) {
+    float x[SCAN_B], gg[SCAN_B];
+#pragma unroll
+    for (int j = 0; j < SCAN_B; ++j) {
+      const bool ok = s0 - j >= 0;
+      x[j] = ok ? __ldcs(dD + base + (long long)(s0 - j) * D * D) : 0.f;
+      gg[j] = ok ? __ldg(gm + (s0 - j) * D) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < SCAN_B; ++j) {
+      if (s0 - j >= 0) {
+        Dend[base + (long long)(s0 - j) * D * D] = run;
+        run = expf(gg[j]) * run + x[j];
+        if (vv == 0) cumGr[(long long)(hh * nseg + s0 - j) * D + c] = cm;
+        cm += gg[j];
+      }
     }
   }
+  if (ds0) ds0[((long long)hh * D + c) * D + vv] = run;
 }
 
 // ============================================================== K3: forward outputs

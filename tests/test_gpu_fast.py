@@ -125,3 +125,35 @@ def test_fast_zero_cotangent_gives_zero_grads():
     got = run_fast(q, k, v, g, np.zeros_like(do), 2)
     for key in ("dq", "dk", "dv", "dg"):
         assert np.all(got[key] == 0.0), key
+
+
+@pytest.mark.parametrize("h,L", [(160, 128), (37, 192)])
+def test_fast_more_heads_than_sms(h, L):
+    """h > #SMs: one segment per head, more than one CTA wave; odd head count / tile count."""
+    q, k, v, g, do = make_case(h, 1, L, seed=11, long_memory=True)
+    got = run_fast(q, k, v, g, do, 1)
+    for hh in (0, h // 2, h - 1):
+        sl = slice(hh, hh + 1)
+        want = oracle(q[sl], k[sl], v[sl], g[sl], do[sl], 1)
+        check({kk: got[kk][sl] for kk in ("o", "dq", "dk", "dv", "dg")}, want)
+
+
+def test_fast_deterministic_and_linear_in_v_at_cfg2():
+    """Full BASELINE config-2 size: bitwise-deterministic reruns, and o / dq linear in v (fp32-accumulated
+    bf16 path: o(v1) + o(v2) vs o(v1 + v2) within the bf16 tolerance)."""
+    from paper_2507_01004_b200 import ops
+    torch.manual_seed(0)
+    h, L, D = 16, 16384, 128
+    sh = ops.ZecoShard(h, L, D, D, 64, torch.bfloat16)
+    q, k, v1, v2 = ((torch.rand(h, L, D, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(4))
+    g = torch.rand(h, L, D, device="cuda") * (math.log(0.999) - math.log(0.9)) + math.log(0.9)
+
+    def fwd(v):
+        sh.fwd_local(k, v, g)
+        return sh.fwd_output(q, k, v, g).float()
+    a1, a2 = fwd(v1), fwd(v1)
+    assert torch.equal(a1, a2)
+    s = fwd((v1.float() + v2.float()).to(torch.bfloat16))
+    lin = a1 + fwd(v2)
+    err = ((s - lin).norm() / lin.norm()).item()
+    assert err <= TOL_BF16, err
