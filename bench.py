@@ -47,7 +47,7 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
-    p.add_argument("--e2e-groups", type=int, default=8, help="head groups of the host-buffer pipeline")
+    p.add_argument("--e2e-groups", type=int, default=4, help="head groups of the host-buffer pipeline")
     p.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     return p.parse_args()
 
@@ -326,10 +326,12 @@ def main():
     d2h = sum(x.numel() * x.element_size() for x in host_out)
 
     def e2e_step():
-        # the public host-buffer call: heads pipelined H2D -> kernels -> D2H on three streams
-        layer.forward_backward_host(host_in, host_out, head_groups=args.e2e_groups)
+        # the public host-buffer call: heads pipelined H2D -> kernels -> D2H on three streams; consecutive
+        # steps chain (step i+1's H2D runs under step i's D2H); host_wait() closes the timed region
+        layer.forward_backward_host(host_in, host_out, head_groups=args.e2e_groups, overlap=True)
 
     e2e_step()
+    layer.host_wait()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -337,6 +339,7 @@ def main():
     e0.record(stream)
     for _ in range(args.e2e_steps):
         e2e_step()
+    layer.host_wait()
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
@@ -382,7 +385,7 @@ def main():
         "e2e": {"value": world * L / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                 "call": f"ZecoRank.forward_backward_host -> zgla_zeco_fwd_bwd_host, pinned host buffers, "
-                        f"{args.e2e_groups} head groups pipelined H2D/kernels/D2H"},
+                        f"{args.e2e_groups} head groups pipelined H2D/kernels/D2H, consecutive steps chained"},
         "gpu_launches": args.steps * (6 + (4 if world > 1 else 0)),
         "clocks": clk.summary(),
     }

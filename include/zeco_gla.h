@@ -132,13 +132,19 @@ int zgla_allscan_info(const zgla_allscan_comm* c, int* rank, int* world, int* he
  * groups pipelined over three streams (H2D / kernels / D2H), so transfers in both directions
  * overlap each other and the kernels.  comm may be NULL (one rank); otherwise it must have been
  * created for heads / head_groups heads and every rank runs the groups in the same order.
- * dev_buf: device scratch of zgla_zeco_fwd_bwd_host_bytes() bytes.  Stream-ordered: the host
- * outputs are complete when `stream` has drained. */
+ * dev_buf: device scratch of zgla_zeco_fwd_bwd_host_bytes() bytes.
+ * flags = 0: stream-ordered; the host outputs are complete when `stream` has drained.
+ * flags = ZGLA_HOST_OVERLAP: repeated calls with the same geometry and dev_buf chain through
+ *   per-group events, so a call's H2D runs under the previous call's D2H; host inputs are read
+ *   asynchronously (do not modify them until the call completes) and completion is awaited with
+ *   zgla_zeco_host_wait(stream), which makes `stream` wait for the last call's D2H. */
+#define ZGLA_HOST_OVERLAP 1
 long long zgla_zeco_fwd_bwd_host_bytes(const zgla_shape* s, int num_sms, int head_groups);
 int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head_groups, zgla_allscan_comm* comm,
                            int num_blocks, const void* q, const void* k, const void* v, const void* g,
                            const void* d_out, void* o, void* dq, void* dk, void* dv, void* dg, void* dev_buf,
-                           long long dev_buf_bytes, void* stream);
+                           long long dev_buf_bytes, int flags, void* stream);
+int zgla_zeco_host_wait(void* stream);
 
 /* ---- diagnostics -------------------------------------------------------- */
 /* record per-tile pipeline timestamps (%globaltimer) of CTA `cta` of the fused kernels into

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libzeco_gla.so")
 
 ZGLA_BF16, ZGLA_F32, ZGLA_F64 = 0, 1, 2
 ZGLA_FWD, ZGLA_BWD = 0, 1
+ZGLA_HOST_OVERLAP = 1
 
 _CODES = {
     -1: errors.DimsError,
@@ -72,7 +73,8 @@ _SIGS = {
     "zgla_allscan_bytes_sent": ([_P], _LL),
     "zgla_allscan_info": ([_P, _P, _P, _P], _I),
     "zgla_zeco_fwd_bwd_host_bytes": ([ctypes.POINTER(Shape), _I, _I], _LL),
-    "zgla_zeco_fwd_bwd_host": ([ctypes.POINTER(Shape), _I, _I, _P, _I] + [_P] * 11 + [_LL, _P], _I),
+    "zgla_zeco_fwd_bwd_host": ([ctypes.POINTER(Shape), _I, _I, _P, _I] + [_P] * 11 + [_LL, _I, _P], _I),
+    "zgla_zeco_host_wait": ([_P], _I),
     "zgla_set_trace": ([_P, _I], _I),
     "zgla_selftest_tmem": ([_I, _I, _I, _P, _P, _P], _I),
     "zgla_selftest_stream": ([_P, _LL, _I, _I, _I, _I, _I, _P], _I),

@@ -15,6 +15,7 @@
 // With a peer communicator (world > 1) every group runs its own All-Scan on
 // the group's [hg, dk, dv] states; all ranks walk the groups in the same
 // order, so the chain protocol's epochs line up.
+#include <cstdint>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -27,7 +28,11 @@ namespace hostpipe {
 struct Ctx {
   int dev = -1;
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  std::vector<cudaEvent_t> ev;
+  std::vector<cudaEvent_t> ev;  // per group: H2D done, kernels done, D2H done; then start, done
+  // geometry of the last call (ZGLA_HOST_OVERLAP chains only onto an identical previous call)
+  int last_G = 0, last_heads = 0, last_dtype = -1;
+  long long last_L = 0;
+  const void* last_buf = nullptr;
 };
 static std::mutex g_mu;
 static Ctx g_ctx[64];
@@ -49,52 +54,6 @@ static int get_ctx(Ctx** out, size_t nev) {
   }
   *out = &c;
   return ZGLA_OK;
-}
-
-// SM-driven transfers between device memory and pinned (device-mapped) host memory, kept as an
-// option (ZGLA_XFER=sm: both directions, ZGLA_XFER=hyb: SM reads for H2D + DMA for D2H).  Measured
-// on the B200 box (cfg2, 402 MB each way): bidirectional copy-engine DMA loses ~50 us per extra
-// copy pair once transfers are split (1 copy 8.1 ms, 40 copies 10.3 ms, 80 copies 11.2 ms); SM
-// reads of pinned host memory reach ~98 GB/s alone but drop to 25-35 GB/s as soon as any D2H
-// traffic runs concurrently, so whole-call times were 12.7-15 ms against 10.2-10.5 ms with DMA.
-// The default is therefore DMA.
-struct Xfer {
-  const uint4* src[5];
-  uint4* dst[5];
-  long long n16[5];  // 16-byte units per tensor
-  int count;
-};
-// Each direction gets XFER_CTAS whole SMs (1024 threads x 4 x 16 B = 64 KB in flight per SM); the
-// group kernels are planned for the remaining num_sms - 2 * XFER_CTAS SMs, so transfers never wait
-// for a compute wave and vice versa.
-constexpr int XFER_CTAS = 8, XFER_THREADS = 1024, XFER_UNROLL = 4;
-
-__global__ void __launch_bounds__(XFER_THREADS, 1) xfer_kernel(Xfer x) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (int t = 0; t < x.count; ++t) {
-    const uint4* __restrict__ src = x.src[t];
-    uint4* __restrict__ dst = x.dst[t];
-    const long long n = x.n16[t];
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; i + (XFER_UNROLL - 1) * stride < n; i += XFER_UNROLL * stride) {
-      uint4 v[XFER_UNROLL];
-#pragma unroll
-      for (int u = 0; u < XFER_UNROLL; ++u) v[u] = __ldcs(src + i + u * stride);
-#pragma unroll
-      for (int u = 0; u < XFER_UNROLL; ++u) __stcs(dst + i + u * stride, v[u]);
-    }
-    for (; i < n; i += stride) __stcs(dst + i, __ldcs(src + i));
-  }
-}
-
-// host pointer usable by device code (pinned + mapped under UVA)?
-static bool device_mapped(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost && a.devicePointer == p;
 }
 
 inline long long al256(long long x) { return (x + 255) & ~255ll; }
@@ -170,7 +129,7 @@ extern "C" long long zgla_zeco_fwd_bwd_host_bytes(const zgla_shape* s, int num_s
 extern "C" int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head_groups, zgla_allscan_comm* comm,
                                       int num_blocks, const void* q, const void* k, const void* v, const void* g,
                                       const void* d_out, void* o, void* dq, void* dk, void* dv, void* dg,
-                                      void* dev_buf, long long dev_buf_bytes, void* stream) {
+                                      void* dev_buf, long long dev_buf_bytes, int flags, void* stream) {
   if (!s) return ZGLA_ERR_DIMS;
   int rank = 0, world = 1, comm_heads = 0;
   if (comm) {
@@ -194,7 +153,7 @@ extern "C" int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head
   Ctx* cx = nullptr;
   {
     std::lock_guard<std::mutex> lock(g_mu);
-    if (int rc = get_ctx(&cx, 2 * (size_t)G + 2)) return rc;
+    if (int rc = get_ctx(&cx, 3 * (size_t)G + 2)) return rc;
   }
   cudaStream_t st = (cudaStream_t)stream;
   unsigned char* base = reinterpret_cast<unsigned char*>(dev_buf);
@@ -206,53 +165,44 @@ extern "C" int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head
                                L * s->value_dim * e, L * s->key_dim * a};
   const void* hin[5] = {q, k, v, g, d_out};
   void* hout[5] = {o, dq, dk, dv, dg};
-  cudaEvent_t ev_start = cx->ev[2 * G], ev_done = cx->ev[2 * G + 1];
-  // optional SM-driven transfers (every host buffer device-mapped and 16-byte aligned)
-  static const int xmode = [] {  // 0 dma, 1 sm both directions, 2 sm h2d + dma d2h
-    const char* e = std::getenv("ZGLA_XFER");
-    return !e ? 0 : e[0] == 's' ? 1 : e[0] == 'h' ? 2 : 0;
-  }();
-  bool sm_xfer = xmode != 0;
-  for (int i = 0; i < 5 && sm_xfer; ++i)
-    sm_xfer = device_mapped(hin[i]) && device_mapped(hout[i]) &&
-              ((reinterpret_cast<uintptr_t>(hin[i]) | reinterpret_cast<uintptr_t>(hout[i])) & 15) == 0 &&
-              ph_in[i] % 16 == 0 && ph_out[i] % 16 == 0;
+  cudaEvent_t* ev_in = &cx->ev[0];
+  cudaEvent_t* ev_comp = &cx->ev[G];
+  cudaEvent_t* ev_d2h = &cx->ev[2 * G];
+  cudaEvent_t ev_start = cx->ev[3 * G], ev_done = cx->ev[3 * G + 1];
+  // ZGLA_HOST_OVERLAP: chain onto the previous call with the same geometry and buffer through per-group
+  // events only (group j's H2D waits for the previous call's group-j kernels, its kernels for the
+  // previous call's group-j D2H), so this call's H2D runs under the previous call's D2H.  The caller's
+  // stream is then NOT made to wait for the D2H: zgla_zeco_host_wait() does that.
+  const bool chain = (flags & ZGLA_HOST_OVERLAP) && cx->last_G == G && cx->last_buf == dev_buf &&
+                     cx->last_heads == s->heads && cx->last_L == s->seq_len && cx->last_dtype == s->dtype;
   // diagnostics: ZGLA_HOST_TRACE=1 prints the per-group timeline (synchronises; never in timed runs)
   static const bool trace = std::getenv("ZGLA_HOST_TRACE") != nullptr;
   std::vector<cudaEvent_t> tev;
   if (trace) {
     tev.resize(3 * G + 1);
-    for (auto& e : tev) cudaEventCreate(&e);
+    for (auto& x : tev) cudaEventCreate(&x);
     cudaEventRecord(tev[3 * G], st);
   }
-  // the device buffers may still be in use by earlier work on the caller's stream
-  if (cudaError_t r = cudaEventRecord(ev_start, st)) return cuda_fail(r, "zgla_zeco_fwd_bwd_host");
-  cudaStreamWaitEvent(cx->h2d, ev_start, 0);
-  cudaStreamWaitEvent(cx->d2h, ev_start, 0);
-  const int csms = sm_xfer && num_sms > 4 * XFER_CTAS ? num_sms - (xmode == 1 ? 2 : 1) * XFER_CTAS : num_sms;
+  if (!chain) {
+    // the device buffers may still be in use by earlier work on the caller's stream
+    if (cudaError_t r = cudaEventRecord(ev_start, st)) return cuda_fail(r, "zgla_zeco_fwd_bwd_host");
+    cudaStreamWaitEvent(cx->h2d, ev_start, 0);
+    cudaStreamWaitEvent(cx->d2h, ev_start, 0);
+  }
   for (int j = 0; j < G; ++j) {
     const int h0 = gb[j], h1 = gb[j + 1];
     const int hg = h1 - h0;
-    if (sm_xfer) {
-      Xfer x;
-      x.count = 5;
-      for (int i = 0; i < 5; ++i) {
-        x.src[i] = reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(hin[i]) + h0 * ph_in[i]);
-        x.dst[i] = reinterpret_cast<uint4*>(base + lo.in[i] + h0 * ph_in[i]);
-        x.n16[i] = hg * ph_in[i] / 16;
-      }
-      xfer_kernel<<<XFER_CTAS, XFER_THREADS, 0, cx->h2d>>>(x);
-    } else {
-      for (int i = 0; i < 5; ++i) {
-        if (cudaError_t r = cudaMemcpyAsync(base + lo.in[i] + h0 * ph_in[i],
-                                            reinterpret_cast<const unsigned char*>(hin[i]) + h0 * ph_in[i],
-                                            hg * ph_in[i], cudaMemcpyHostToDevice, cx->h2d))
-          return cuda_fail(r, "zgla_zeco_fwd_bwd_host h2d");
-      }
+    if (chain) cudaStreamWaitEvent(cx->h2d, ev_comp[j], 0);  // previous call's kernels of group j
+    for (int i = 0; i < 5; ++i) {
+      if (cudaError_t r = cudaMemcpyAsync(base + lo.in[i] + h0 * ph_in[i],
+                                          reinterpret_cast<const unsigned char*>(hin[i]) + h0 * ph_in[i],
+                                          hg * ph_in[i], cudaMemcpyHostToDevice, cx->h2d))
+        return cuda_fail(r, "zgla_zeco_fwd_bwd_host h2d");
     }
-    cudaEventRecord(cx->ev[2 * j], cx->h2d);
+    cudaEventRecord(ev_in[j], cx->h2d);
     if (trace) cudaEventRecord(tev[3 * j], cx->h2d);
-    cudaStreamWaitEvent(st, cx->ev[2 * j], 0);
+    cudaStreamWaitEvent(st, ev_in[j], 0);
+    if (chain) cudaStreamWaitEvent(st, ev_d2h[j], 0);  // previous call's D2H of group j's outputs
     zgla_shape gs = *s;
     gs.heads = hg;
     void* in[5];
@@ -267,57 +217,63 @@ extern "C" int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head
     float* ds0 = reinterpret_cast<float*>(base + lo.st[4]);
     float* recv_b = reinterpret_cast<float*>(base + lo.st[5]);
     float* scan_b = reinterpret_cast<float*>(base + lo.st[6]);
-    if (int rc = zgla_zeco_fwd_local(&gs, csms, in[1], in[2], in[3], ws, s_local, g_tot, st)) return rc;
+    if (int rc = zgla_zeco_fwd_local(&gs, num_sms, in[1], in[2], in[3], ws, s_local, g_tot, st)) return rc;
     const void* prev = nullptr;
     if (peers) {
       if (int rc = zgla_allscan_run(comm, num_blocks, ZGLA_FWD, s_local, g_tot, recv_f, scan_f, st)) return rc;
       prev = rank > 0 ? recv_f : nullptr;
     }
-    if (int rc = zgla_zeco_fwd_output(&gs, csms, in[0], in[1], in[2], in[3], ws, prev, out[0], st)) return rc;
-    if (int rc = zgla_zeco_bwd_local(&gs, csms, in[0], in[3], in[4], ws, ds0, st)) return rc;
+    if (int rc = zgla_zeco_fwd_output(&gs, num_sms, in[0], in[1], in[2], in[3], ws, prev, out[0], st)) return rc;
+    if (int rc = zgla_zeco_bwd_local(&gs, num_sms, in[0], in[3], in[4], ws, ds0, st)) return rc;
     const void* ds_next = nullptr;
     if (peers) {
       if (int rc = zgla_allscan_run(comm, num_blocks, ZGLA_BWD, ds0, g_tot, recv_b, scan_b, st)) return rc;
       ds_next = rank < world - 1 ? recv_b : nullptr;
     }
-    if (int rc = zgla_zeco_bwd_output(&gs, csms, in[0], in[1], in[2], in[3], in[4], ws, prev, ds_next, out[1],
+    if (int rc = zgla_zeco_bwd_output(&gs, num_sms, in[0], in[1], in[2], in[3], in[4], ws, prev, ds_next, out[1],
                                       out[2], out[3], out[4], st))
       return rc;
-    cudaEventRecord(cx->ev[2 * j + 1], st);
+    cudaEventRecord(ev_comp[j], st);
     if (trace) cudaEventRecord(tev[3 * j + 1], st);
-    cudaStreamWaitEvent(cx->d2h, cx->ev[2 * j + 1], 0);
-    if (sm_xfer && xmode == 1) {
-      Xfer x;
-      x.count = 5;
-      for (int i = 0; i < 5; ++i) {
-        x.src[i] = reinterpret_cast<const uint4*>(base + lo.out[i] + h0 * ph_out[i]);
-        x.dst[i] = reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(hout[i]) + h0 * ph_out[i]);
-        x.n16[i] = hg * ph_out[i] / 16;
-      }
-      xfer_kernel<<<XFER_CTAS, XFER_THREADS, 0, cx->d2h>>>(x);
-    } else {
-      for (int i = 0; i < 5; ++i) {
-        if (cudaError_t r = cudaMemcpyAsync(reinterpret_cast<unsigned char*>(hout[i]) + h0 * ph_out[i],
-                                            base + lo.out[i] + h0 * ph_out[i], hg * ph_out[i],
-                                            cudaMemcpyDeviceToHost, cx->d2h))
-          return cuda_fail(r, "zgla_zeco_fwd_bwd_host d2h");
-      }
+    cudaStreamWaitEvent(cx->d2h, ev_comp[j], 0);
+    for (int i = 0; i < 5; ++i) {
+      if (cudaError_t r = cudaMemcpyAsync(reinterpret_cast<unsigned char*>(hout[i]) + h0 * ph_out[i],
+                                          base + lo.out[i] + h0 * ph_out[i], hg * ph_out[i],
+                                          cudaMemcpyDeviceToHost, cx->d2h))
+        return cuda_fail(r, "zgla_zeco_fwd_bwd_host d2h");
     }
+    cudaEventRecord(ev_d2h[j], cx->d2h);
     if (trace) cudaEventRecord(tev[3 * j + 2], cx->d2h);
   }
-  // completion of the caller's stream implies the host outputs are written
   cudaEventRecord(ev_done, cx->d2h);
-  cudaStreamWaitEvent(st, ev_done, 0);
+  const bool overlap = (flags & ZGLA_HOST_OVERLAP) != 0;
+  if (!overlap) cudaStreamWaitEvent(st, ev_done, 0);  // completion of the caller's stream => outputs written
+  cx->last_G = G;
+  cx->last_buf = dev_buf;
+  cx->last_heads = s->heads;
+  cx->last_L = s->seq_len;
+  cx->last_dtype = s->dtype;
   if (trace) {
     cudaDeviceSynchronize();
     for (int j = 0; j < G; ++j) {
-      float a, b, c;
-      cudaEventElapsedTime(&a, tev[3 * G], tev[3 * j]);
-      cudaEventElapsedTime(&b, tev[3 * G], tev[3 * j + 1]);
-      cudaEventElapsedTime(&c, tev[3 * G], tev[3 * j + 2]);
-      std::fprintf(stderr, "zgla host trace group %d: h2d %.3f compute %.3f d2h %.3f ms\n", j, a, b, c);
+      float t0, t1, t2;
+      cudaEventElapsedTime(&t0, tev[3 * G], tev[3 * j]);
+      cudaEventElapsedTime(&t1, tev[3 * G], tev[3 * j + 1]);
+      cudaEventElapsedTime(&t2, tev[3 * G], tev[3 * j + 2]);
+      std::fprintf(stderr, "zgla host trace group %d: h2d %.3f compute %.3f d2h %.3f ms\n", j, t0, t1, t2);
     }
-    for (auto& e : tev) cudaEventDestroy(e);
+    for (auto& x : tev) cudaEventDestroy(x);
   }
   return zgla_check_launch();
+}
+
+extern "C" int zgla_zeco_host_wait(void* stream) {
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return cuda_fail(e, "zgla_zeco_host_wait");
+  std::lock_guard<std::mutex> lock(g_mu);
+  Ctx& c = g_ctx[dev];
+  if (c.dev < 0 || c.ev.empty() || c.last_G <= 0) return ZGLA_OK;
+  if (cudaError_t e = cudaStreamWaitEvent((cudaStream_t)stream, c.ev[3 * c.last_G + 1], 0))
+    return cuda_fail(e, "zgla_zeco_host_wait");
+  return ZGLA_OK;
 }

@@ -141,11 +141,13 @@ class ZecoRank:
         self._prev, self._g_tot = prev, g_tot
         return self.shard.fwd_output(q, k, v, g, prev, out=out)
 
-    def forward_backward_host(self, host_in, host_out, head_groups=16):
+    def forward_backward_host(self, host_in, host_out, head_groups=16, overlap=False):
         """One layer forward + backward with inputs (q, k, v, g, dO) and outputs (o, dq, dk, dv, dg) in
         HOST memory (CPU torch tensors, pinned for full PCIe rate), through the C-ABI call
         ``zgla_zeco_fwd_bwd_host``: heads are pipelined in ``head_groups`` groups so host->device,
-        kernels and device->host overlap.  Stream-ordered on the current stream."""
+        kernels and device->host overlap.  Stream-ordered on the current stream; with ``overlap=True``
+        consecutive calls chain (a call's H2D runs under the previous call's D2H) and completion is
+        awaited with ``host_wait()``."""
         geo = self.shard.geo
         names = ("q", "k", "v", "g", "d_out", "o", "dq", "dk", "dv", "dg")
         acc = geo.acc
@@ -175,10 +177,15 @@ class ZecoRank:
                 cache[head_groups] = AllScanP2P(geo.h // head_groups, geo.dk, geo.dv, group=self.comm.group)
             comm = cache[head_groups]._h
         _native.call("zgla_zeco_fwd_bwd_host", ctypes.byref(self.shard.shape), self.shard.sms, head_groups, comm,
-                     self.K, *(ctypes.c_void_p(t.data_ptr()) for t in ts), ops._p(buf), buf.numel(), ops._stream())
+                     self.K, *(ctypes.c_void_p(t.data_ptr()) for t in ts), ops._p(buf), buf.numel(),
+                     _native.ZGLA_HOST_OVERLAP if overlap else 0, ops._stream())
         if self.world > 1:
             self.ledger[("all_scan", "sent")] += geo.h * geo.dk * geo.dv * (
                 (self.rank < self.world - 1) + (self.rank > 0))
+
+    def host_wait(self):
+        """Make the current stream wait for the last forward_backward_host(overlap=True) call's D2H."""
+        _native.call("zgla_zeco_host_wait", ops._stream())
 
     def backward(self, q, k, v, g, d_out, grads=None):
         ds0 = self.shard.bwd_local(q, g, d_out)

@@ -87,3 +87,26 @@ def test_host_call_rejects_bad_args():
         layer.forward_backward_host(host, out, head_groups=5)
     with pytest.raises(ConfigError):
         layer.forward_backward_host([x.cuda() for x in host], out, head_groups=1)
+
+
+def test_host_call_overlap_chain_matches():
+    """overlap=True: consecutive calls chained through per-group events give the same results as the
+    stream-ordered call once host_wait() has been honoured (inputs changed between calls)."""
+    from paper_2507_01004_b200 import distributed as zd
+    h, L, D = 4, 512, 128
+    layer = zd.ZecoRank(h, L, D, 64, torch.bfloat16)
+    cases = [_case(h, L, D, torch.bfloat16, seed=s) for s in (1, 2, 3)]
+    want = []
+    for host in cases:
+        out = _outs(h, L, D, torch.bfloat16)
+        layer.forward_backward_host(host, out, head_groups=2)
+        torch.cuda.current_stream().synchronize()
+        want.append(out)
+    outs = [_outs(h, L, D, torch.bfloat16) for _ in cases]
+    for host, out in zip(cases, outs):
+        layer.forward_backward_host(host, out, head_groups=2, overlap=True)
+    layer.host_wait()
+    torch.cuda.current_stream().synchronize()
+    for a_set, b_set in zip(outs, want):
+        for a, b in zip(a_set, b_set):
+            assert torch.equal(a, b)
