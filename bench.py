@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--e2e-groups", type=int, default=4, help="head groups of the host-buffer pipeline")
     p.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    p.add_argument("--same-device", action="store_true",
+                   help="validation only: all ranks on cuda:0 with a gloo bootstrap (timings meaningless)")
     return p.parse_args()
 
 
@@ -222,10 +224,20 @@ def main():
     import torch
     import torch.distributed as dist
 
+    if args.same_device:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], device="cpu" if args.same_device else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     from paper_2507_01004_b200 import distributed as zd
 
@@ -313,9 +325,7 @@ def main():
         dist.barrier()
     ms = start.elapsed_time(end)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms)
     ms_step = ms / args.steps
     value = world * L / (ms_step / 1e3)
 
@@ -344,9 +354,7 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(e2e_ms)
 
     # ---- roofline of the dominant kernel (bwd_out_kernel) and of the whole step
     hbm, tc_peak, peak_kind = peaks()

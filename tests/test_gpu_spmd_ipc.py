@@ -1,0 +1,21 @@
+"""The multi-GPU code path (AllScanP2P: CUDA-IPC handle exchange, peer stores, flags, acks, epochs)
+run by 2 processes sharing this GPU (gloo bootstrap); bitwise equal to the single-process list form."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_ipc_allscan_two_processes_one_gpu(P):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29611 + P),
+           os.path.join(ROOT, "scripts", "spmd_ipc_check.py"), "--same-device", "--rounds", "2"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=400, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "SPMD IPC check OK" in r.stdout
