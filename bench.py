@@ -294,9 +294,9 @@ def main():
         step(e)
     torch.cuda.synchronize()
     per_phase = {p: statistics.mean(e[j].elapsed_time(e[j + 1]) for e in evs) for j, p in enumerate(phases)}
-    # the timed region: the step captured once as a CUDA graph (N=1; with peers the All-Scan
-    # kernels carry host-side epochs, so N>1 replays eager launches) and replayed K times
-    use_graph = world == 1 and not args.no_graph
+    # the timed region: the step captured once as a CUDA graph and replayed K times (with peers too:
+    # the All-Scan chain keeps its epochs in device memory, so replays advance the protocol)
+    use_graph = not args.no_graph
     graph = None
     if use_graph:
         side = torch.cuda.Stream()

@@ -231,9 +231,20 @@ __global__ void __launch_bounds__(kThreads) local_chain_kernel(int P, int h, int
 }
 
 // SPMD form: one rank per process
-__global__ void __launch_bounds__(kThreads) rank_chain_kernel(Link<float> L, int h, int dk, int dv, int K, unsigned epoch,
-                                                              int* err) {
+// The epoch lives in device memory (ctl[0]) so that a captured CUDA graph replays correctly: every
+// CTA reads the completed-call count at entry (the previous call on this stream has finished), and the
+// last CTA to leave publishes the new count (ctl[1] counts departures).
+__global__ void __launch_bounds__(kThreads) rank_chain_kernel(Link<float> L, int h, int dk, int dv, int K,
+                                                              unsigned* ctl, int* err) {
+  const unsigned epoch = *reinterpret_cast<volatile unsigned*>(ctl) + 1;
   rank_body<float, true>(L, h, dk, dv, K, blockIdx.x, gridDim.x, epoch, err);  // peers: system scope
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ctl + 1, 1u) == gridDim.x - 1) {
+      ctl[1] = 0;
+      *reinterpret_cast<volatile unsigned*>(ctl) = epoch;
+    }
+  }
 }
 
 // list-form workspace (flags + error word), grown on demand
@@ -290,8 +301,7 @@ struct zgla_allscan_comm {
   unsigned char* next_region;
   unsigned char* prev_region;
   bool next_ipc, prev_ipc;
-  unsigned epoch[2];
-  int* err;
+  int* err;  // [0] deadlock flag; [2 + 2 d], [3 + 2 d]: per-direction device epoch and departure count
   long long bytes_sent;
 };
 
@@ -326,7 +336,6 @@ extern "C" int zgla_allscan_create(int rank, int world, int heads, int key_dim, 
   c->max_blocks = max_blocks;
   c->nel = (long long)heads * key_dim * value_dim;
   c->region_bytes = 2 * dir_bytes(c);
-  c->epoch[0] = c->epoch[1] = 0;
   c->bytes_sent = 0;
   c->next_region = c->prev_region = nullptr;
   c->next_ipc = c->prev_ipc = false;
@@ -335,12 +344,12 @@ extern "C" int zgla_allscan_create(int rank, int world, int heads, int key_dim, 
     return cuda_fail(e, "zgla_allscan_create");
   }
   cudaMemset(c->region, 0, c->region_bytes);
-  if (cudaError_t e = cudaMalloc(&c->err, sizeof(int))) {
+  if (cudaError_t e = cudaMalloc(&c->err, 8 * sizeof(int))) {
     cudaFree(c->region);
     delete c;
     return cuda_fail(e, "zgla_allscan_create");
   }
-  cudaMemset(c->err, 0, sizeof(int));
+  cudaMemset(c->err, 0, 8 * sizeof(int));
   if (cudaError_t e = cudaDeviceSynchronize()) return cuda_fail(e, "zgla_allscan_create");
   *out = c;
   return ZGLA_OK;
@@ -397,7 +406,6 @@ extern "C" int zgla_allscan_run(zgla_allscan_comm* c, int num_blocks, int direct
   unsigned char* succ = d == ZGLA_FWD ? c->next_region : c->prev_region;
   unsigned char* pred = d == ZGLA_FWD ? c->prev_region : c->next_region;
   if ((!is_sink && !succ) || (!is_source && !pred)) return ZGLA_ERR_STATE;  // not bound
-  const unsigned epoch = ++c->epoch[d];
   Link<float> L;
   L.local = local_state;
   L.logdecay = log_decay;
@@ -412,7 +420,8 @@ extern "C" int zgla_allscan_run(zgla_allscan_comm* c, int num_blocks, int direct
   L.recv_out = recv;
   L.scanned_out = scanned;
   if (c->world == 1) L.inbox = nullptr;
-  rank_chain_kernel<<<kCtasPerRank, kThreads, 0, st>>>(L, c->h, c->dk, c->dv, num_blocks, epoch, c->err);
+  unsigned* ctl = reinterpret_cast<unsigned*>(c->err) + 2 + 2 * d;
+  rank_chain_kernel<<<kCtasPerRank, kThreads, 0, st>>>(L, c->h, c->dk, c->dv, num_blocks, ctl, c->err);
   if (int rc = zgla_check_launch()) return rc;
   if (!is_sink) c->bytes_sent += c->nel * (long long)sizeof(float);
   return zgla_check_launch();

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--heads", type=int, default=2)
     ap.add_argument("--seq", type=int, default=512, help="tokens per rank")
     ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--graph", action="store_true", help="capture fwd+bwd once as a CUDA graph and replay it")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", 0 if args.same_device else int(os.environ.get("LOCAL_RANK", 0)))
@@ -43,9 +44,23 @@ def main():
     g, do = part(g_full, rank), part(do_full, rank)
     comm = zd.AllScanP2P(H, D, D)
     layer = zd.ZecoRank(H, L, D, 64, torch.bfloat16, comm=comm, num_blocks=4)
-    for _ in range(args.rounds):  # epochs advance; inboxes / acks are reused across calls
-        o = layer.forward(q, k, v, g)
-        grads = layer.backward(q, k, v, g, do)
+    o = torch.empty_like(q)
+    grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty_like(g))
+
+    def step():
+        layer.forward(q, k, v, g, out=o)
+        layer.backward(q, k, v, g, do, grads=grads)
+    step()
+    torch.cuda.synchronize()
+    if args.graph:  # replays must advance the chain's device-side epochs
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        for _ in range(args.rounds):
+            graph.replay()
+    else:
+        for _ in range(args.rounds):  # epochs advance; inboxes / acks are reused across calls
+            step()
     torch.cuda.synchronize()
     res = torch.cat([o.float().cpu().flatten()] + [x.float().cpu().flatten() for x in grads])
     gathered = [torch.empty_like(res) for _ in range(world)] if rank == 0 else None

@@ -11,11 +11,11 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("P", [2, 3])
-def test_ipc_allscan_two_processes_one_gpu(P):
+@pytest.mark.parametrize("P,graph", [(2, False), (3, False), (2, True)])
+def test_ipc_allscan_two_processes_one_gpu(P, graph):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29611 + P),
-           os.path.join(ROOT, "scripts", "spmd_ipc_check.py"), "--same-device", "--rounds", "2"]
+           "--master-addr", "127.0.0.1", "--master-port", str(29611 + P + 10 * graph),
+           os.path.join(ROOT, "scripts", "spmd_ipc_check.py"), "--same-device", "--rounds", "2"] + (["--graph"] if graph else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=400, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "SPMD IPC check OK" in r.stdout
