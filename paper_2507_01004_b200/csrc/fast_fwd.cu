@@ -500,29 +500,40 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       const long long sidx = (long long)(hh * nseg + s) * D * D + c;  // column-major workspace state
       const float cg = s_prev ? expf(cumG[(hh * nseg + s) * D + c]) : 0.f;
       const float* pv = s_prev ? s_prev + ((long long)hh * D + c) * D : nullptr;
+      // all loads first (two batches of 64 values, straight into TMEM); the bf16 copy S' needs the first
+      // tile's reference point, so it is written from TMEM once the prep warps have published it
+#pragma unroll 1
+      for (int q2 = 0; q2 < 4; q2 += 2) {
+        float v[2][32];
+#pragma unroll
+        for (int hq = 0; hq < 2; ++hq) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const int col = 32 * (q2 + hq) + j;
+            float4 a = make_float4(Sin[sidx + col * D], Sin[sidx + (col + 1) * D], Sin[sidx + (col + 2) * D],
+                                   Sin[sidx + (col + 3) * D]);
+            if (pv) {
+              const float4 b = *reinterpret_cast<const float4*>(pv + col);
+              a.x += cg * b.x;
+              a.y += cg * b.y;
+              a.z += cg * b.z;
+              a.w += cg * b.w;
+            }
+            v[hq][j] = a.x;
+            v[hq][j + 1] = a.y;
+            v[hq][j + 2] = a.z;
+            v[hq][j + 3] = a.w;
+          }
+        }
+        tmem_st32(s_addr + 32 * q2, v[0]);
+        tmem_st32(s_addr + 32 * (q2 + 1), v[1]);
+      }
       mbar_wait(&prep[0], 0);
       const float e0 = fast_exp(vr[c]);
 #pragma unroll 1
       for (int q = 0; q < 4; ++q) {
         float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          const int col = 32 * q + j;
-          float4 a = make_float4(Sin[sidx + col * D], Sin[sidx + (col + 1) * D], Sin[sidx + (col + 2) * D],
-                                 Sin[sidx + (col + 3) * D]);
-          if (pv) {
-            const float4 b = *reinterpret_cast<const float4*>(pv + 32 * q + j);
-            a.x += cg * b.x;
-            a.y += cg * b.y;
-            a.z += cg * b.z;
-            a.w += cg * b.w;
-          }
-          v[j] = a.x;
-          v[j + 1] = a.y;
-          v[j + 2] = a.z;
-          v[j + 3] = a.w;
-        }
-        tmem_st32(s_addr + 32 * q, v);
+        tmem_ld32(s_addr + 32 * q, v);
         write_sp(v, q, e0);
       }
     }

@@ -157,3 +157,18 @@ def test_fast_deterministic_and_linear_in_v_at_cfg2():
     lin = a1 + fwd(v2)
     err = ((s - lin).norm() / lin.norm()).item()
     assert err <= TOL_BF16, err
+
+
+@pytest.mark.parametrize("lo,hi", [(math.log(0.5), math.log(0.9)), (math.log(0.2), math.log(0.5))])
+def test_fast_strong_decay_inside_domain(lo, hi):
+    """Strong gates (per-token decay down to 0.2: 64-token tile log-decay down to about -103, in-tile
+    exponents up to ~52) stay inside the fast path's overflow-free domain (tile log-decay > -170)."""
+    h, P, L = 2, 2, 512
+    q, k, v, g = orc.make_inputs(P, L, h, 128, 128, 5, lo, hi)
+    do = orc.make_cotangent(5, h, P * L, 128)
+    q, k, v, do = (bf16_round(x) for x in (q, k, v, do))
+    g = g.astype(np.float32).astype(np.float64)
+    got = run_fast(q, k, v, g, do, P)
+    for key in ("o", "dq", "dk", "dv", "dg"):
+        assert np.all(np.isfinite(got[key])), key
+    check(got, oracle(q, k, v, g, do, P))
