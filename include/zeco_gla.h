@@ -50,6 +50,16 @@ typedef struct {
   int dtype;         /* ZGLA_BF16 / ZGLA_F32 / ZGLA_F64 */
 } zgla_shape;
 
+/* A [heads][tokens][channels] tensor with arbitrary token and head strides (in ELEMENTS; channels
+ * contiguous).  0 means dense (channels, resp. tokens * channels).  Lets the ZeCO entry points read
+ * and write views such as the head slices of a token-major [tokens][heads * channels] projection
+ * output without a transposing copy (fused tcgen05 path; the SIMT paths need dense tensors). */
+typedef struct {
+  void* data;
+  long long token_stride;
+  long long head_stride;
+} zgla_tensor;
+
 /* ---- library ----------------------------------------------------------- */
 const char* zgla_version(void);
 const char* zgla_last_error(void);
@@ -101,6 +111,20 @@ int zgla_zeco_bwd_local(const zgla_shape* s, int num_sms, const void* q, const v
 int zgla_zeco_bwd_output(const zgla_shape* s, int num_sms, const void* q, const void* k, const void* v,
                          const void* g, const void* d_out, void* ws, const void* s_prev, const void* ds_next,
                          void* dq, void* dk, void* dv, void* dg, void* stream);
+
+/* the same four entry points over strided tensors (zgla_tensor); ZGLA_ERR_LAYOUT if a stride or base is
+ * not 16-byte aligned, or if the shape runs the SIMT path and a tensor is not dense */
+int zgla_zeco_fwd_local_v(const zgla_shape* s, int num_sms, const zgla_tensor* k, const zgla_tensor* v,
+                          const zgla_tensor* g, void* ws, void* s_local, void* g_tot, void* stream);
+int zgla_zeco_fwd_output_v(const zgla_shape* s, int num_sms, const zgla_tensor* q, const zgla_tensor* k,
+                           const zgla_tensor* v, const zgla_tensor* g, void* ws, const void* s_prev,
+                           const zgla_tensor* o, void* stream);
+int zgla_zeco_bwd_local_v(const zgla_shape* s, int num_sms, const zgla_tensor* q, const zgla_tensor* g,
+                          const zgla_tensor* d_out, void* ws, void* ds_local0, void* stream);
+int zgla_zeco_bwd_output_v(const zgla_shape* s, int num_sms, const zgla_tensor* q, const zgla_tensor* k,
+                           const zgla_tensor* v, const zgla_tensor* g, const zgla_tensor* d_out, void* ws,
+                           const void* s_prev, const void* ds_next, const zgla_tensor* dq, const zgla_tensor* dk,
+                           const zgla_tensor* dv, const zgla_tensor* dg, void* stream);
 
 /* ---- All-Scan (glasp/collectives.py:70-140) ----------------------------- */
 /* All P "ranks" resident on one device (the reference's list form): one kernel runs the

@@ -42,7 +42,13 @@ class Shape(ctypes.Structure):
     ]
 
 
+class Tensor(ctypes.Structure):
+    """zgla_tensor: [heads][tokens][channels] view with element strides (0 = dense)."""
+    _fields_ = [("data", ctypes.c_void_p), ("token_stride", ctypes.c_longlong), ("head_stride", ctypes.c_longlong)]
+
+
 _P = ctypes.c_void_p
+_T = ctypes.POINTER(Tensor)
 _I = ctypes.c_int
 _LL = ctypes.c_longlong
 _SIGS = {
@@ -63,6 +69,10 @@ _SIGS = {
     "zgla_zeco_fwd_output": ([ctypes.POINTER(Shape), _I, _P, _P, _P, _P, _P, _P, _P, _P], _I),
     "zgla_zeco_bwd_local": ([ctypes.POINTER(Shape), _I, _P, _P, _P, _P, _P, _P], _I),
     "zgla_zeco_bwd_output": ([ctypes.POINTER(Shape), _I] + [_P] * 13, _I),
+    "zgla_zeco_fwd_local_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _P, _P, _P, _P], _I),
+    "zgla_zeco_fwd_output_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _T, _P, _P, _T, _P], _I),
+    "zgla_zeco_bwd_local_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _P, _P, _P], _I),
+    "zgla_zeco_bwd_output_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _T, _T, _P, _P, _P, _T, _T, _T, _T, _P], _I),
     "zgla_allscan_local": ([_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P], _I),
     "zgla_allscan_create": ([_I, _I, _I, _I, _I, _I, ctypes.POINTER(_P)], _I),
     "zgla_allscan_export": ([_P, _P], _I),

@@ -4,6 +4,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "fast_common.cuh"
 #include "zgla_internal.h"
 
 namespace zgla {
@@ -32,15 +33,21 @@ int generic_zeco_bwd_output(const zgla_shape*, const void*, const void*, const v
                             void*, const void*, const void*, void*, void*, void*, void*, cudaStream_t);
 long long generic_ws_bytes(const zgla_shape*);
 
-// provided by fast_fwd.cu / fast_bwd.cu
+// provided by fast_fwd.cu / fast_bwd.cu (strided tensors)
+namespace fast {
+struct TRef;
+}
 bool fast_supported(const zgla_shape* s);
 long long fast_ws_bytes(const zgla_shape* s, int num_sms);
-int fast_fwd_local(const zgla_shape*, int, const void*, const void*, const void*, void*, void*, void*, cudaStream_t);
-int fast_fwd_output(const zgla_shape*, int, const void*, const void*, const void*, const void*, void*, const void*,
-                    void*, cudaStream_t);
-int fast_bwd_local(const zgla_shape*, int, const void*, const void*, const void*, void*, void*, cudaStream_t);
-int fast_bwd_output(const zgla_shape*, int, const void*, const void*, const void*, const void*, const void*, void*,
-                    const void*, const void*, void*, void*, void*, void*, cudaStream_t);
+int fast_fwd_local(const zgla_shape*, int, const fast::TRef&, const fast::TRef&, const fast::TRef&, void*, void*,
+                   void*, cudaStream_t);
+int fast_fwd_output(const zgla_shape*, int, const fast::TRef&, const fast::TRef&, const fast::TRef&,
+                    const fast::TRef&, void*, const void*, const fast::TRef&, cudaStream_t);
+int fast_bwd_local(const zgla_shape*, int, const fast::TRef&, const fast::TRef&, const fast::TRef&, void*, void*,
+                   cudaStream_t);
+int fast_bwd_output(const zgla_shape*, int, const fast::TRef&, const fast::TRef&, const fast::TRef&,
+                    const fast::TRef&, const fast::TRef&, void*, const void*, const void*, const fast::TRef&,
+                    const fast::TRef&, const fast::TRef&, const fast::TRef&, cudaStream_t);
 
 }  // namespace zgla
 
@@ -77,36 +84,110 @@ extern "C" long long zgla_zeco_workspace_bytes(const zgla_shape* s, int num_sms)
   return fast_supported(s) ? fast_ws_bytes(s, num_sms) : generic_ws_bytes(s);
 }
 
+// ---- ZeCO entry points: strided (zgla_tensor) forms; the pointer forms below are dense wrappers
+static bool dense(const zgla_tensor* t, const zgla_shape* s, int width) {
+  return (t->token_stride == 0 || t->token_stride == width) &&
+         (t->head_stride == 0 || s->heads == 1 || t->head_stride == s->seq_len * width);
+}
+// fast path: every tensor 16-byte aligned with aligned strides; SIMT path: dense tensors only
+static int check_refs(const zgla_shape* s, std::initializer_list<const zgla_tensor*> ts, bool fast_path) {
+  for (const zgla_tensor* t : ts) {
+    if (!t || !t->data) return ZGLA_ERR_DIMS;
+    if (fast_path) {
+      if (!fast::ref_ok(fast::as_ref(t, s->seq_len, s->heads), 2)) {
+        set_error("strided tensor: base and strides must be 16-byte aligned, token stride >= channels");
+        return ZGLA_ERR_LAYOUT;
+      }
+    } else if (!dense(t, s, s->key_dim) && !dense(t, s, s->value_dim)) {
+      set_error("the SIMT (non-bf16 / non-128) path needs dense [heads][tokens][channels] tensors");
+      return ZGLA_ERR_LAYOUT;
+    }
+  }
+  return ZGLA_OK;
+}
+
+extern "C" int zgla_zeco_fwd_local_v(const zgla_shape* s, int num_sms, const zgla_tensor* k, const zgla_tensor* v,
+                                     const zgla_tensor* g, void* ws, void* s_local, void* g_tot, void* stream) {
+  if (int rc = validate_zeco(s, num_sms)) return rc;
+  const bool fp = fast_supported(s);
+  if (int rc = check_refs(s, {k, v, g}, fp)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long L = s->seq_len;
+  if (fp)
+    return fast_fwd_local(s, num_sms, fast::as_ref(k, L, s->heads), fast::as_ref(v, L, s->heads), fast::as_ref(g, L, s->heads), ws, s_local, g_tot,
+                          st);
+  return generic_zeco_fwd_local(s, k->data, v->data, g->data, ws, s_local, g_tot, st);
+}
+
+extern "C" int zgla_zeco_fwd_output_v(const zgla_shape* s, int num_sms, const zgla_tensor* q, const zgla_tensor* k,
+                                      const zgla_tensor* v, const zgla_tensor* g, void* ws, const void* s_prev,
+                                      const zgla_tensor* o, void* stream) {
+  if (int rc = validate_zeco(s, num_sms)) return rc;
+  const bool fp = fast_supported(s);
+  if (int rc = check_refs(s, {q, k, v, g, o}, fp)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long L = s->seq_len;
+  if (fp)
+    return fast_fwd_output(s, num_sms, fast::as_ref(q, L, s->heads), fast::as_ref(k, L, s->heads), fast::as_ref(v, L, s->heads),
+                           fast::as_ref(g, L, s->heads), ws, s_prev, fast::as_ref(o, L, s->heads), st);
+  return generic_zeco_fwd_output(s, q->data, k->data, v->data, g->data, ws, s_prev, o->data, st);
+}
+
+extern "C" int zgla_zeco_bwd_local_v(const zgla_shape* s, int num_sms, const zgla_tensor* q, const zgla_tensor* g,
+                                     const zgla_tensor* d_out, void* ws, void* ds_local0, void* stream) {
+  if (int rc = validate_zeco(s, num_sms)) return rc;
+  const bool fp = fast_supported(s);
+  if (int rc = check_refs(s, {q, g, d_out}, fp)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long L = s->seq_len;
+  if (fp)
+    return fast_bwd_local(s, num_sms, fast::as_ref(q, L, s->heads), fast::as_ref(g, L, s->heads), fast::as_ref(d_out, L, s->heads), ws, ds_local0,
+                          st);
+  return generic_zeco_bwd_local(s, q->data, g->data, d_out->data, ws, ds_local0, st);
+}
+
+extern "C" int zgla_zeco_bwd_output_v(const zgla_shape* s, int num_sms, const zgla_tensor* q, const zgla_tensor* k,
+                                      const zgla_tensor* v, const zgla_tensor* g, const zgla_tensor* d_out, void* ws,
+                                      const void* s_prev, const void* ds_next, const zgla_tensor* dq,
+                                      const zgla_tensor* dk, const zgla_tensor* dv, const zgla_tensor* dg,
+                                      void* stream) {
+  if (int rc = validate_zeco(s, num_sms)) return rc;
+  const bool fp = fast_supported(s);
+  if (int rc = check_refs(s, {q, k, v, g, d_out, dq, dk, dv, dg}, fp)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long L = s->seq_len;
+  if (fp)
+    return fast_bwd_output(s, num_sms, fast::as_ref(q, L, s->heads), fast::as_ref(k, L, s->heads), fast::as_ref(v, L, s->heads),
+                           fast::as_ref(g, L, s->heads), fast::as_ref(d_out, L, s->heads), ws, s_prev, ds_next, fast::as_ref(dq, L, s->heads),
+                           fast::as_ref(dk, L, s->heads), fast::as_ref(dv, L, s->heads), fast::as_ref(dg, L, s->heads), st);
+  return generic_zeco_bwd_output(s, q->data, k->data, v->data, g->data, d_out->data, ws, s_prev, ds_next, dq->data,
+                                 dk->data, dv->data, dg->data, st);
+}
+
+static zgla_tensor dn(const void* p) { return zgla_tensor{const_cast<void*>(p), 0, 0}; }
+
 extern "C" int zgla_zeco_fwd_local(const zgla_shape* s, int num_sms, const void* k, const void* v, const void* g,
                                    void* ws, void* s_local, void* g_tot, void* stream) {
-  if (int rc = validate_zeco(s, num_sms)) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (fast_supported(s)) return fast_fwd_local(s, num_sms, k, v, g, ws, s_local, g_tot, st);
-  return generic_zeco_fwd_local(s, k, v, g, ws, s_local, g_tot, st);
+  const zgla_tensor tk = dn(k), tv = dn(v), tg = dn(g);
+  return zgla_zeco_fwd_local_v(s, num_sms, &tk, &tv, &tg, ws, s_local, g_tot, stream);
 }
 
 extern "C" int zgla_zeco_fwd_output(const zgla_shape* s, int num_sms, const void* q, const void* k, const void* v,
                                     const void* g, void* ws, const void* s_prev, void* o, void* stream) {
-  if (int rc = validate_zeco(s, num_sms)) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (fast_supported(s)) return fast_fwd_output(s, num_sms, q, k, v, g, ws, s_prev, o, st);
-  return generic_zeco_fwd_output(s, q, k, v, g, ws, s_prev, o, st);
+  const zgla_tensor tq = dn(q), tk = dn(k), tv = dn(v), tg = dn(g), to = dn(o);
+  return zgla_zeco_fwd_output_v(s, num_sms, &tq, &tk, &tv, &tg, ws, s_prev, &to, stream);
 }
 
 extern "C" int zgla_zeco_bwd_local(const zgla_shape* s, int num_sms, const void* q, const void* g,
                                    const void* d_out, void* ws, void* ds_local0, void* stream) {
-  if (int rc = validate_zeco(s, num_sms)) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (fast_supported(s)) return fast_bwd_local(s, num_sms, q, g, d_out, ws, ds_local0, st);
-  return generic_zeco_bwd_local(s, q, g, d_out, ws, ds_local0, st);
+  const zgla_tensor tq = dn(q), tg = dn(g), td = dn(d_out);
+  return zgla_zeco_bwd_local_v(s, num_sms, &tq, &tg, &td, ws, ds_local0, stream);
 }
 
 extern "C" int zgla_zeco_bwd_output(const zgla_shape* s, int num_sms, const void* q, const void* k, const void* v,
                                     const void* g, const void* d_out, void* ws, const void* s_prev,
                                     const void* ds_next, void* dq, void* dk, void* dv, void* dg, void* stream) {
-  if (int rc = validate_zeco(s, num_sms)) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (fast_supported(s))
-    return fast_bwd_output(s, num_sms, q, k, v, g, d_out, ws, s_prev, ds_next, dq, dk, dv, dg, st);
-  return generic_zeco_bwd_output(s, q, k, v, g, d_out, ws, s_prev, ds_next, dq, dk, dv, dg, st);
+  const zgla_tensor tq = dn(q), tk = dn(k), tv = dn(v), tg = dn(g), td = dn(d_out);
+  const zgla_tensor a = dn(dq), b = dn(dk), c = dn(dv), e = dn(dg);
+  return zgla_zeco_bwd_output_v(s, num_sms, &tq, &tk, &tv, &tg, &td, ws, s_prev, ds_next, &a, &b, &c, &e, stream);
 }

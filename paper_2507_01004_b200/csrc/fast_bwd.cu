@@ -44,16 +44,17 @@ constexpr size_t BO_SMEM = 1024 + BO_OFF_BAR + 256;
 // LB holds d = logb - r per (channel lane, token column), double buffered, written by the prep warps.
 constexpr uint32_t BC_DQ = 0, BC_DK = 64, BC_DV = 128, BC_QDO = 192, BC_SC = 320, BC_LB = 384;
 
+template <bool DENSE>
 __global__ void __launch_bounds__(BO_THREADS, 1)
     bwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                    const __grid_constant__ CUtensorMap tm_sp, const __grid_constant__ CUtensorMap tm_g,
-                   const float* __restrict__ g, long long L, int nseg,
+                   const float* __restrict__ g, long long gts, long long ghs, long long L, int in3d, int nseg,
                    int ntiles, const float* __restrict__ Sin, const float* __restrict__ cumG,
                    const float* __restrict__ dS, const float* __restrict__ gamseg, const float* __restrict__ s_prev,
                    const float* __restrict__ Dend, const float* __restrict__ cumGr,
                    const float* __restrict__ ds_next, __nv_bfloat16* __restrict__ dq, __nv_bfloat16* __restrict__ dk,
-                   __nv_bfloat16* __restrict__ dv, float* __restrict__ dg, unsigned long long* trace,
+                   __nv_bfloat16* __restrict__ dv, float* __restrict__ dg, Strides4 gs, unsigned long long* trace,
                    int trace_cta) {
   extern __shared__ uint8_t smem_raw[];
   // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
@@ -91,9 +92,12 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   int t0, t1;
   seg_range(s, nseg, ntiles, t0, t1);
   const int nt = t1 - t0;
-  const int row0 = (int)(hh * L);
   unsigned long long* tr = (trace != nullptr && (int)blockIdx.x == trace_cta) ? trace : nullptr;
   if (trace != nullptr && threadIdx.x == 0) cta_trace_begin(trace);
+  if constexpr (DENSE) {  // compile-time strides for the dense layout
+    gts = D, ghs = L * D;
+    gs = Strides4{D, D, D, D, L * D, L * D, L * D, L * D};
+  }
 
   if (tid == 0) {
     for (int i = 0; i < BO_NS; ++i) {
@@ -133,38 +137,21 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_do);
       tma_prefetch_desc(&tm_sp);
-      for (int i = 0; i < nt + PF_DIST; ++i) {
-        if (PF_DIST > 0 && i < nt) {
-          const int r = row0 + (t1 - 1 - i) * T;
-          tma_prefetch_2d(&tm_q, 0, r);
-          tma_prefetch_2d(&tm_q, 64, r);
-          tma_prefetch_2d(&tm_k, 0, r);
-          tma_prefetch_2d(&tm_k, 64, r);
-          tma_prefetch_2d(&tm_v, 0, r);
-          tma_prefetch_2d(&tm_v, 64, r);
-          tma_prefetch_2d(&tm_do, 0, r);
-          tma_prefetch_2d(&tm_do, 64, r);
-          tma_prefetch_2d(&tm_g, 0, r);
-          const int rs = (hh * ntiles + (t1 - 1 - i)) * D;
-          tma_prefetch_2d(&tm_sp, 0, rs);
-          tma_prefetch_2d(&tm_sp, 64, rs);
-        }
-        const int m = i - PF_DIST;
-        if (m < 0) continue;
+      for (int m = 0; m < nt; ++m) {
         const int st = m % BO_NS, ph = (m / BO_NS) & 1;
         const int n = t1 - 1 - m;
         uint8_t* sb = smem + st * BO_STAGE;
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], BO_STAGE);
-        const int r = row0 + n * T;
-        tma_load_2d(sb, &tm_q, &full[st], 0, r);
-        tma_load_2d(sb + PANEL, &tm_q, &full[st], 64, r);
-        tma_load_2d(sb + TILE_BF16, &tm_k, &full[st], 0, r);
-        tma_load_2d(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r);
-        tma_load_2d(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r);
-        tma_load_2d(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r);
-        tma_load_2d(sb + 3 * TILE_BF16, &tm_do, &full[st], 0, r);
-        tma_load_2d(sb + 3 * TILE_BF16 + PANEL, &tm_do, &full[st], 64, r);
+        const int r = n * T;
+        tile_load<DENSE>(sb, &tm_q, &full[st], 0, r, hh, L, in3d);
+        tile_load<DENSE>(sb + PANEL, &tm_q, &full[st], 64, r, hh, L, in3d);
+        tile_load<DENSE>(sb + TILE_BF16, &tm_k, &full[st], 0, r, hh, L, in3d);
+        tile_load<DENSE>(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r, hh, L, in3d);
+        tile_load<DENSE>(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r, hh, L, in3d);
+        tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d);
+        tile_load<DENSE>(sb + 3 * TILE_BF16, &tm_do, &full[st], 0, r, hh, L, in3d);
+        tile_load<DENSE>(sb + 3 * TILE_BF16 + PANEL, &tm_do, &full[st], 64, r, hh, L, in3d);
         mbar_wait(sp_empty, (m & 1) ^ 1);
         mbar_arrive_expect_tx(sp_full, STATE_BF16);
         const int rs = (hh * ntiles + n) * D;
@@ -251,9 +238,15 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const int n = t1 - 1 - m;
       uint8_t* sb = smem + st * BO_STAGE;
       float lb[64];
-      const float* gp = g + ((long long)row0 + n * T) * D + c;
+      const float* gp = g + hh * ghs + (long long)n * T * gts + c;
 #pragma unroll
-      for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);
+      if constexpr (DENSE) {
+        for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);  // immediate offsets
+      } else {
+        const float* pr = gp;  // runtime stride: one pointer bump per row keeps the loads back to back
+#pragma unroll
+        for (int r = 0; r < 64; ++r, pr += gts) lb[r] = __ldg(pr);
+      }
 #pragma unroll
       for (int r = 1; r < 64; ++r) lb[r] += lb[r - 1];
       const float rr = lb[31];
@@ -415,10 +408,13 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const uint8_t* sb = smem + st * BO_STAGE;
       const uint32_t cols = 32 * ch;
       const uint32_t lbcol = BC_LB + 64 * (m & 1) + cols;
-      const long long tok0 = (long long)row0 + n * T + cols;
+      const long long tok0 = (long long)n * T + cols;  // token index inside the head
       constexpr float LOG2E = 1.4426950408889634f;
       float da[32];
       float tsum = 0.f;
+      __nv_bfloat16* pdq = dq + hh * gs.qh + tok0 * gs.qt + c;
+      __nv_bfloat16* pdk = dk + hh * gs.kh + tok0 * gs.kt + c;
+      __nv_bfloat16* pdv = dv + hh * gs.vh + tok0 * gs.vt + c;
 #pragma unroll
       for (int h8 = 0; h8 < 4; ++h8) {
         uint32_t gq[8], gk[8], gv8[8], dl[8];
@@ -444,9 +440,10 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           da[i] = qh[u] * q_raw - kh[u] * k_raw;
           tsum += da[i];
 #ifndef ZGLA_EXP_NOSTORE
-          dq[(tok0 + i) * D + c] = __float2bfloat16_rn(q_raw * fast_exp2(dlt));
-          dk[(tok0 + i) * D + c] = __float2bfloat16_rn(k_raw * fast_exp2(-dlt));
-          dv[(tok0 + i) * D + c] = __float2bfloat16_rn(__uint_as_float(gv8[u]));
+          *pdq = __float2bfloat16_rn(q_raw * fast_exp2(dlt));
+          *pdk = __float2bfloat16_rn(k_raw * fast_exp2(-dlt));
+          *pdv = __float2bfloat16_rn(__uint_as_float(gv8[u]));
+          pdq += gs.qt, pdk += gs.kt, pdv += gs.vt;
 #else
           if (q_raw * fast_exp2(dlt) + k_raw * fast_exp2(-dlt) + __uint_as_float(gv8[u]) == 1234.5f) dq[0] = 0;
 #endif
@@ -461,10 +458,11 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const float rho_end = xr[c];
       const float t_upper = xcarry[D + c], t_lower = xcarry[c];
       float base = rho_end + (ch == 0 ? t_lower + t_upper : t_upper);
+      float* pdg = dg + hh * gs.gh + tok0 * gs.gt + c;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < 32; ++i, pdg += gs.gt) {
 #ifndef ZGLA_EXP_NOSTORE
-        dg[(tok0 + i) * D + c] = base;
+        *pdg = base;
 #else
         if (base == 1234.5f) dg[0] = 0;
 #endif
@@ -486,25 +484,30 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
 
 using namespace fast;
 
-int fast_bwd_output(const zgla_shape* s, int num_sms, const void* q, const void* k, const void* v, const void* g,
-                    const void* d_out, void* ws, const void* s_prev, const void* ds_next, void* dq, void* dk,
-                    void* dv, void* dg, cudaStream_t st) {
+int fast_bwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef& k, const TRef& v, const TRef& g,
+                    const TRef& d_out, void* ws, const void* s_prev, const void* ds_next, const TRef& dq,
+                    const TRef& dk, const TRef& dv, const TRef& dg, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
   CUtensorMap mq, mk, mv, mdo, msp, mg;
-  const unsigned long long rows = (unsigned long long)pl.h * pl.L;
-  if (int rc = make_map(&mq, q, true, rows, D, 64, T, true)) return rc;
-  if (int rc = make_map(&mk, k, true, rows, D, 64, T, true)) return rc;
-  if (int rc = make_map(&mv, v, true, rows, D, 64, T, true)) return rc;
-  if (int rc = make_map(&mdo, d_out, true, rows, D, 64, T, true)) return rc;
+  const bool din = is_dense(q, pl.L) && is_dense(k, pl.L) && is_dense(v, pl.L) && is_dense(d_out, pl.L);
+  const bool dn = is_dense(g, pl.L) && is_dense(dq, pl.L) && is_dense(dk, pl.L) && is_dense(dv, pl.L) &&
+                  is_dense(dg, pl.L);
+  if (int rc = map_act(&mq, q, pl.L, pl.h, din)) return rc;
+  if (int rc = map_act(&mk, k, pl.L, pl.h, din)) return rc;
+  if (int rc = map_act(&mv, v, pl.L, pl.h, din)) return rc;
+  if (int rc = map_act(&mdo, d_out, pl.L, pl.h, din)) return rc;
   if (int rc = make_map(&msp, w.Sp, true, (unsigned long long)pl.h * pl.ntiles * D, D, 64, D, true)) return rc;
-  if (int rc = make_map(&mg, g, false, rows, D, D, T, false)) return rc;
-  set_smem_once((const void*)bwd_out_kernel, (int)BO_SMEM);
-  if (cudaError_t e = launch_k(bwd_out_kernel, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp, mg,
-                                (const float*)g, pl.L, pl.nseg, pl.ntiles, (const float*)w.Sin, (const float*)w.cumG,
-                                (const float*)w.dS, (const float*)w.gam, (const float*)s_prev, (const float*)w.Dend,
-                                (const float*)w.cumGr, (const float*)ds_next, (__nv_bfloat16*)dq,
-                                (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, (float*)dg, g_trace_buf, g_trace_cta))
+  if (int rc = map_gate(&mg, g, pl.L, pl.h, din && is_dense(g, pl.L))) return rc;
+  const Strides4 gs{(int)dq.ts, (int)dk.ts, (int)dv.ts, (int)dg.ts, dq.hs, dk.hs, dv.hs, dg.hs};
+  auto kern = dn ? bwd_out_kernel<true> : bwd_out_kernel<false>;
+  set_smem_once((const void*)kern, (int)BO_SMEM);
+  if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp, mg,
+                                (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, pl.nseg, pl.ntiles,
+                                (const float*)w.Sin, (const float*)w.cumG, (const float*)w.dS, (const float*)w.gam, (const float*)s_prev,
+                                (const float*)w.Dend, (const float*)w.cumGr, (const float*)ds_next,
+                                (__nv_bfloat16*)dq.p, (__nv_bfloat16*)dk.p, (__nv_bfloat16*)dv.p, (float*)dg.p, gs,
+                                g_trace_buf, g_trace_cta))
     return cuda_fail(e, "bwd_out_kernel");
   return zgla_check_launch();
 }

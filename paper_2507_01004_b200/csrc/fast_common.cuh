@@ -27,7 +27,6 @@ constexpr int TILE_BF16 = T * D * 2;   // 16 KiB
 constexpr int TILE_F32 = T * D * 4;    // 32 KiB
 constexpr int SPANEL = D * 128;        // one 64-column panel of a [D x D] bf16 state (16 KiB)
 constexpr int STATE_BF16 = D * D * 2;  // 32 KiB
-constexpr int PF_DIST = 0;             // tiles of L2 prefetch ahead of the smem pipeline (measured: hurts)
 
 struct Plan {
   int h, nseg, ntiles;
@@ -127,6 +126,77 @@ inline int make_map(CUtensorMap* m, const void* base, bool bf16, unsigned long l
     return ZGLA_ERR_CUDA;
   }
   return ZGLA_OK;
+}
+
+// a [heads][tokens][D] tensor with arbitrary token / head strides (elements; channels contiguous)
+struct TRef {
+  const void* p;
+  long long ts;  // token stride
+  long long hs;  // head stride
+};
+// token / head strides of the four gradient outputs of the backward kernel (elements)
+struct Strides4 {  // token strides fit in 32 bits (fewer live registers in the epilogue); head strides not
+  int qt, kt, vt, gt;
+  long long qh, kh, vh, gh;
+};
+inline TRef dense_ref(const void* p, long long L) { return TRef{p, D, L * D}; }
+inline TRef as_ref(const zgla_tensor* t, long long L, int heads) {
+  // a single head's head stride is irrelevant: normalise it so dense single-head views stay dense
+  return TRef{t->data, t->token_stride ? t->token_stride : D,
+              (t->head_stride && heads > 1) ? t->head_stride : L * D};
+}
+// TMA needs 16-byte aligned bases and strides; channel rows are 16-byte vectors for the stores
+inline bool ref_ok(const TRef& r, int esize) {
+  return r.p && (reinterpret_cast<uintptr_t>(r.p) & 15) == 0 && (r.ts * esize) % 16 == 0 &&
+         (r.hs * esize) % 16 == 0 && r.ts >= D && r.ts < (1ll << 31) && r.hs >= 0;
+}
+
+// 3-D map (channels, tokens, heads) over a strided [heads][tokens][D] tensor; box = box_cols x box_rows x 1
+inline int make_map3(CUtensorMap* m, const TRef& r, bool bf16, long long L, int heads, unsigned box_cols,
+                     unsigned box_rows, bool swizzle128) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return ZGLA_ERR_CUDA;
+  }
+  const unsigned eb = bf16 ? 2 : 4;
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)L, (cuuint64_t)heads};
+  cuuint64_t strides[2] = {(cuuint64_t)(r.ts * eb), (cuuint64_t)((r.hs ? r.hs : L * D) * eb)};
+  cuuint32_t box[3] = {box_cols, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult e = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                  const_cast<void*>(r.p), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (e != CUDA_SUCCESS) {
+    char buf[128];
+    std::snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled (3-D) failed (%d)", (int)e);
+    set_error(buf);
+    return ZGLA_ERR_CUDA;
+  }
+  return ZGLA_OK;
+}
+inline bool is_dense(const TRef& r, long long L) { return r.ts == D && r.hs == L * D; }
+inline int map_act(CUtensorMap* m, const TRef& r, long long L, int heads, bool dense) {  // bf16 64x64 SW128
+  if (dense) return make_map(m, r.p, true, (unsigned long long)heads * L, D, 64, T, true);
+  return make_map3(m, r, true, L, heads, 64, T, true);
+}
+inline int map_gate(CUtensorMap* m, const TRef& r, long long L, int heads, bool dense) {  // fp32 128x64 boxes
+  if (dense) return make_map(m, r.p, false, (unsigned long long)heads * L, D, D, T, false);
+  return make_map3(m, r, false, L, heads, D, T, false);
+}
+
+// tile load of (channel col, token t) of head hh: dense tensors use 2-D maps over [h * L] rows,
+// strided ones 3-D maps (channels, tokens, heads)
+// (the map's dimensionality is a launch argument: strided TMA inputs cost nothing measurable, unlike
+// runtime strides in the pointer-addressed g loads and output stores, which select the kernel variant)
+template <bool DENSE>
+__device__ __forceinline__ void tile_load(void* dst, const CUtensorMap* m, uint64_t* bar, int col, int t, int hh,
+                                          long long L, int in3d) {
+  if (!in3d)
+    tma_load_2d(dst, m, bar, col, (int)(hh * L + t));
+  else
+    tma_load_3d(dst, m, bar, col, t, hh);
 }
 
 // ---- optional pipeline tracing (diagnostics): CTA g_trace_cta records %globaltimer per (event, tile)

@@ -28,10 +28,10 @@ constexpr int KS_THREADS = 320;                     // 8 prep warps (2 groups), 
 constexpr int KS_OFF_BAR = KS_NS * KS_STAGE;
 constexpr size_t KS_SMEM = 1024 + KS_NS * KS_STAGE + 4096;
 
-template <int DIR>  // 0: forward local state (a=k, b=v, reverse walk); 1: backward (a=q, b=dO, forward walk)
+template <int DIR, bool DENSE>  // 0: forward local state (a=k, b=v, reverse walk); 1: backward (a=q, b=dO)
 __global__ void __launch_bounds__(KS_THREADS, 1)
     seg_state_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                     const __grid_constant__ CUtensorMap tm_g, long long L, int nseg, int ntiles,
+                     const __grid_constant__ CUtensorMap tm_g, long long L, int in3d, int nseg, int ntiles,
                      float* __restrict__ out_state, float* __restrict__ out_gam) {
   extern __shared__ uint8_t smem_raw[];
   // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
@@ -50,7 +50,6 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
   int t0, t1;
   seg_range(s, nseg, ntiles, t0, t1);
   const int nt = t1 - t0;
-  const int row0 = (int)(hh * L);
 
   if (tid == 0) {
     for (int i = 0; i < KS_NS; ++i) {
@@ -78,29 +77,18 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
       tma_prefetch_desc(&tm_a);
       tma_prefetch_desc(&tm_b);
       tma_prefetch_desc(&tm_g);
-      for (int i = 0; i < nt + PF_DIST; ++i) {
-        if (PF_DIST > 0 && i < nt) {
-          const int tile = DIR == 0 ? t1 - 1 - i : t0 + i;
-          const int r = row0 + tile * T;
-          tma_prefetch_2d(&tm_a, 0, r);
-          tma_prefetch_2d(&tm_a, 64, r);
-          tma_prefetch_2d(&tm_b, 0, r);
-          tma_prefetch_2d(&tm_b, 64, r);
-          tma_prefetch_2d(&tm_g, 0, r);
-        }
-        const int j = i - PF_DIST;  // tile whose shared-memory load is issued now
-        if (j < 0) continue;
+      for (int j = 0; j < nt; ++j) {
         const int st = j % KS_NS, ph = (j / KS_NS) & 1;
         const int tile = DIR == 0 ? t1 - 1 - j : t0 + j;
         uint8_t* sa = smem + st * KS_STAGE;
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], KS_STAGE);
-        const int r = row0 + tile * T;
-        tma_load_2d(sa, &tm_a, &full[st], 0, r);
-        tma_load_2d(sa + PANEL, &tm_a, &full[st], 64, r);
-        tma_load_2d(sa + TILE_BF16, &tm_b, &full[st], 0, r);
-        tma_load_2d(sa + TILE_BF16 + PANEL, &tm_b, &full[st], 64, r);
-        tma_load_2d(sa + 2 * TILE_BF16, &tm_g, &full[st], 0, r);
+        const int r = tile * T;
+        tile_load<DENSE>(sa, &tm_a, &full[st], 0, r, hh, L, in3d);
+        tile_load<DENSE>(sa + PANEL, &tm_a, &full[st], 64, r, hh, L, in3d);
+        tile_load<DENSE>(sa + TILE_BF16, &tm_b, &full[st], 0, r, hh, L, in3d);
+        tile_load<DENSE>(sa + TILE_BF16 + PANEL, &tm_b, &full[st], 64, r, hh, L, in3d);
+        tile_load<DENSE>(sa + 2 * TILE_BF16, &tm_g, &full[st], 0, r, hh, L, in3d);
       }
     }
   } else if (warp == 9) {
@@ -271,12 +259,14 @@ constexpr size_t FO_SMEM = 1024 + FO_OFF_BAR + 256;
 // TMEM columns
 constexpr uint32_t COL_KV = 0, COL_O = 128, COL_A = 256, COL_S = 320;
 
+template <bool DENSE>
 __global__ void __launch_bounds__(FO_THREADS, 1)
     fwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g,
-                   const __grid_constant__ CUtensorMap tm_sp, const float* __restrict__ g, long long L,
-                   int nseg, int ntiles, const float* __restrict__ Sin, const float* __restrict__ cumG,
-                   const float* __restrict__ s_prev, __nv_bfloat16* __restrict__ out,
+                   const __grid_constant__ CUtensorMap tm_sp, const float* __restrict__ g, long long gts,
+                   long long ghs, long long L, int in3d, int nseg, int ntiles, const float* __restrict__ Sin,
+                   const float* __restrict__ cumG, const float* __restrict__ s_prev,
+                   __nv_bfloat16* __restrict__ out, long long ots, long long ohs,
                    __nv_bfloat16* __restrict__ sp_save, unsigned long long* trace, int trace_cta) {
   extern __shared__ uint8_t smem_raw[];
   // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
@@ -305,9 +295,12 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   int t0, t1;
   seg_range(s, nseg, ntiles, t0, t1);
   const int nt = t1 - t0;
-  const int row0 = (int)(hh * L);
   unsigned long long* tr = (trace != nullptr && (int)blockIdx.x == trace_cta) ? trace : nullptr;
   if (trace != nullptr && threadIdx.x == 0) cta_trace_begin(trace);
+  if constexpr (DENSE) {  // compile-time strides for the dense layout
+    gts = D, ots = D;
+    ghs = L * D, ohs = L * D;
+  }
 
   if (tid == 0) {
     for (int i = 0; i < FO_NS; ++i) {
@@ -343,30 +336,18 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_g);
-      for (int i = 0; i < nt + PF_DIST; ++i) {
-        if (PF_DIST > 0 && i < nt) {
-          const int r = row0 + (t0 + i) * T;
-          tma_prefetch_2d(&tm_q, 0, r);
-          tma_prefetch_2d(&tm_q, 64, r);
-          tma_prefetch_2d(&tm_k, 0, r);
-          tma_prefetch_2d(&tm_k, 64, r);
-          tma_prefetch_2d(&tm_v, 0, r);
-          tma_prefetch_2d(&tm_v, 64, r);
-          tma_prefetch_2d(&tm_g, 0, r);
-        }
-        const int n = i - PF_DIST;
-        if (n < 0) continue;
+      for (int n = 0; n < nt; ++n) {
         const int st = n % FO_NS, ph = (n / FO_NS) & 1;
         uint8_t* sb = smem + st * FO_STAGE;
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], FO_STAGE);
-        const int r = row0 + (t0 + n) * T;
-        tma_load_2d(sb, &tm_q, &full[st], 0, r);
-        tma_load_2d(sb + PANEL, &tm_q, &full[st], 64, r);
-        tma_load_2d(sb + TILE_BF16, &tm_k, &full[st], 0, r);
-        tma_load_2d(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r);
-        tma_load_2d(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r);
-        tma_load_2d(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r);
+        const int r = (t0 + n) * T;
+        tile_load<DENSE>(sb, &tm_q, &full[st], 0, r, hh, L, in3d);
+        tile_load<DENSE>(sb + PANEL, &tm_q, &full[st], 64, r, hh, L, in3d);
+        tile_load<DENSE>(sb + TILE_BF16, &tm_k, &full[st], 0, r, hh, L, in3d);
+        tile_load<DENSE>(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r, hh, L, in3d);
+        tile_load<DENSE>(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r, hh, L, in3d);
+        tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d);
         ZTRACE(tr, 0, n);
       }
     }
@@ -442,9 +423,15 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       const int st = n % FO_NS, ph = (n / FO_NS) & 1;
       uint8_t* sb = smem + st * FO_STAGE;
       float lb[64];
-      const float* gp = g + ((long long)row0 + (t0 + n) * T) * D + c;
+      const float* gp = g + hh * ghs + (long long)(t0 + n) * T * gts + c;
 #pragma unroll
-      for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);
+      if constexpr (DENSE) {
+        for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);  // immediate offsets
+      } else {
+        const float* pr = gp;  // runtime stride: one pointer bump per row keeps the loads back to back
+#pragma unroll
+        for (int r = 0; r < 64; ++r, pr += gts) lb[r] = __ldg(pr);
+      }
 #pragma unroll
       for (int r = 1; r < 64; ++r) lb[r] += lb[r - 1];
       const float rr = lb[31];
@@ -614,7 +601,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         tmem_ld32(taddr(tbase, 32 * qd, COL_O + 32 * q), o);
         if ((lane >> 4) == ob) {
           const int i = 16 * qd + (lane & 15);
-          uint4* dst = reinterpret_cast<uint4*>(out + ((long long)row0 + (t0 + n) * T + i) * D + 32 * q);
+          uint4* dst = reinterpret_cast<uint4*>(out + hh * ohs + ((long long)(t0 + n) * T + i) * ots + 32 * q);
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
             uint4 w;
@@ -649,28 +636,22 @@ bool fast_supported(const zgla_shape* s) {
 
 long long fast_ws_bytes(const zgla_shape* s, int num_sms) { return ws_bytes(make_plan(s, num_sms)); }
 
-static int map_bf16(CUtensorMap* m, const void* p, const Plan& pl) {
-  return make_map(m, p, true, (unsigned long long)pl.h * pl.L, D, 64, T, true);
-}
-static int map_f32(CUtensorMap* m, const void* p, const Plan& pl) {
-  return make_map(m, p, false, (unsigned long long)pl.h * pl.L, D, D, T, false);
-}
-
-int launch_seg_state(int dir, const Plan& pl, const void* a, const void* b, const void* g, float* out_state,
+int launch_seg_state(int dir, const Plan& pl, const TRef& a, const TRef& b, const TRef& g, float* out_state,
                      float* out_gam, cudaStream_t st) {
   CUtensorMap ma, mb, mg;
-  if (int rc = map_bf16(&ma, a, pl)) return rc;
-  if (int rc = map_bf16(&mb, b, pl)) return rc;
-  if (int rc = map_f32(&mg, g, pl)) return rc;
-  auto kern = dir == 0 ? seg_state_kernel<0> : seg_state_kernel<1>;
+  const bool dn = is_dense(a, pl.L) && is_dense(b, pl.L) && is_dense(g, pl.L);  // all TMA-read
+  if (int rc = map_act(&ma, a, pl.L, pl.h, dn)) return rc;
+  if (int rc = map_act(&mb, b, pl.L, pl.h, dn)) return rc;
+  if (int rc = map_gate(&mg, g, pl.L, pl.h, dn)) return rc;
+  auto kern = dir == 0 ? seg_state_kernel<0, true> : seg_state_kernel<1, true>;
   set_smem_once((const void*)kern, (int)KS_SMEM);
-  if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, KS_THREADS, KS_SMEM, st, ma, mb, mg, pl.L, pl.nseg,
+  if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, KS_THREADS, KS_SMEM, st, ma, mb, mg, pl.L, dn ? 0 : 1, pl.nseg,
                                 pl.ntiles, out_state, out_gam))
     return cuda_fail(e, "seg_state_kernel");
   return zgla_check_launch();
 }
 
-int fast_fwd_local(const zgla_shape* s, int num_sms, const void* k, const void* v, const void* g, void* ws,
+int fast_fwd_local(const zgla_shape* s, int num_sms, const TRef& k, const TRef& v, const TRef& g, void* ws,
                    void* s_local, void* g_tot, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
@@ -682,25 +663,32 @@ int fast_fwd_local(const zgla_shape* s, int num_sms, const void* k, const void* 
   return zgla_check_launch();
 }
 
-int fast_fwd_output(const zgla_shape* s, int num_sms, const void* q, const void* k, const void* v, const void* g,
-                    void* ws, const void* s_prev, void* o, cudaStream_t st) {
+int fast_fwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef& k, const TRef& v, const TRef& g,
+                    void* ws, const void* s_prev, const TRef& o, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
   CUtensorMap mq, mk, mv, mg, msp;
+  // maps: 2-D iff the TMA-read inputs are dense; kernel variant: compile-time strides iff the
+  // pointer-addressed tensors (g, o) are dense
+  const bool din = is_dense(q, pl.L) && is_dense(k, pl.L) && is_dense(v, pl.L);
+  const bool dn = is_dense(g, pl.L) && is_dense(o, pl.L);
   if (int rc = make_map(&msp, w.Sp, true, (unsigned long long)pl.h * pl.ntiles * D, D, 64, D, true)) return rc;
-  if (int rc = map_bf16(&mq, q, pl)) return rc;
-  if (int rc = map_bf16(&mk, k, pl)) return rc;
-  if (int rc = map_bf16(&mv, v, pl)) return rc;
-  if (int rc = map_f32(&mg, g, pl)) return rc;
-  set_smem_once((const void*)fwd_out_kernel, (int)FO_SMEM);
-  if (cudaError_t e = launch_k(fwd_out_kernel, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
-                                (const float*)g, pl.L, pl.nseg, pl.ntiles, (const float*)w.Sin, (const float*)w.cumG,
-                                (const float*)s_prev, (__nv_bfloat16*)o, w.Sp, g_trace_buf, g_trace_cta))
+  if (int rc = map_act(&mq, q, pl.L, pl.h, din)) return rc;
+  if (int rc = map_act(&mk, k, pl.L, pl.h, din)) return rc;
+  if (int rc = map_act(&mv, v, pl.L, pl.h, din)) return rc;
+  if (int rc = map_gate(&mg, g, pl.L, pl.h, din && is_dense(g, pl.L))) return rc;
+  auto kern = dn ? fwd_out_kernel<true> : fwd_out_kernel<false>;
+  set_smem_once((const void*)kern, (int)FO_SMEM);
+  if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
+                                (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, pl.nseg, pl.ntiles,
+                                (const float*)w.Sin, (const float*)w.cumG, (const float*)s_prev, (__nv_bfloat16*)o.p,
+                                o.ts, o.hs, w.Sp,
+                                g_trace_buf, g_trace_cta))
     return cuda_fail(e, "fwd_out_kernel");
   return zgla_check_launch();
 }
 
-int fast_bwd_local(const zgla_shape* s, int num_sms, const void* q, const void* g, const void* d_out, void* ws,
+int fast_bwd_local(const zgla_shape* s, int num_sms, const TRef& q, const TRef& g, const TRef& d_out, void* ws,
                    void* ds0, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);

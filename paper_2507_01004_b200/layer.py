@@ -7,10 +7,10 @@ this module is the wrapper a training stack needs around the hot path:
   points (glasp/engine.py:218-237 forward, 348-364 backward): local scan ->
   All-Scan FWD -> outputs with the fused correction; local reverse scan ->
   All-Scan BWD -> gradients with the fused corrections.  Tensors are
-  head-major ``[h, L, d]`` (the reference layout, glasp/gla.py:29-30); the
-  per-call ZecoShard workspace (segment states, saved chunk states) is kept
+  ``[h, L, d]`` (the reference layout, glasp/gla.py:29-30) and may be strided views of
+  token-major buffers (zgla_tensor strides, no transposing copies); the per-call ZecoShard workspace (segment states, saved chunk states) is kept
   on the autograd context from forward to backward.
-* ``GatedLinearAttention`` -- hidden -> q, k, v, r (one GEMM, head-major copies),
+* ``GatedLinearAttention`` -- hidden -> q, k, v, r (one GEMM; the kernels read its head slices in place),
   low-rank log-sigmoid gate (g < 0 by construction), ZeCO GLA core, per-head
   RMS norm, swish output gate, output projection.
 * ``GLAModel`` -- embedding, N x (RMSNorm -> GLA -> residual, RMSNorm ->
@@ -45,7 +45,8 @@ class ZecoGLAFunction(torch.autograd.Function):
     def forward(ctx, q, k, v, g, chunk_len, comm, num_blocks):
         h, L, dk = q.shape
         dv = v.shape[2]
-        q, k, v, g = (x.contiguous() for x in (q, k, v, g))
+        # strided [h, L, d] views (e.g. head slices of token-major projections) are read in place
+        q, k, v, g = (x if x.stride(2) == 1 else x.contiguous() for x in (q, k, v, g))
         shard = ops.ZecoShard(h, L, dk, dv, chunk_len, q.dtype, device=q.device)
         s_loc, g_tot = shard.fwd_local(k, v, g)
         prev = None
@@ -54,7 +55,10 @@ class ZecoGLAFunction(torch.autograd.Function):
         if world > 1:
             recv, _ = comm(s_loc, g_tot, num_blocks, _native.ZGLA_FWD)
             prev = recv if rank > 0 else None
-        o = shard.fwd_output(q, k, v, g, prev)
+        # outputs and gradients are produced token-major ([L, h, d] storage, [h, L, d] views), the layout the
+        # surrounding GEMMs consume: the runtime-stride kernel variant costs ~10 % of the core
+        # (scripts/strided_bench.py) but saves the transposing copies (GLA-1.3B step 2.06 -> 1.87 s)
+        o = shard.fwd_output(q, k, v, g, prev, out=_token_major(h, L, dv, q.dtype, q.device))
         ctx.save_for_backward(q, k, v, g)
         ctx.shard, ctx.prev, ctx.g_tot = shard, prev, g_tot
         ctx.comm, ctx.K, ctx.world, ctx.rank = comm, num_blocks, world, rank
@@ -64,15 +68,25 @@ class ZecoGLAFunction(torch.autograd.Function):
     def backward(ctx, d_out):
         q, k, v, g = ctx.saved_tensors
         shard = ctx.shard
-        d_out = d_out.contiguous().to(q.dtype)
+        d_out = d_out.to(q.dtype)
+        if d_out.stride(2) != 1:
+            d_out = d_out.contiguous()
         ds0 = shard.bwd_local(q, g, d_out)
         ds_next = None
         if ctx.world > 1:
             recv, _ = ctx.comm(ds0, ctx.g_tot, ctx.K, _native.ZGLA_BWD)
             ds_next = recv if ctx.rank < ctx.world - 1 else None
-        dq, dk, dv, dg = shard.bwd_output(q, k, v, g, d_out, ctx.prev, ds_next)
+        h, L, dk_, dv_ = q.shape[0], q.shape[1], q.shape[2], v.shape[2]
+        grads = (_token_major(h, L, dk_, q.dtype, q.device), _token_major(h, L, dk_, q.dtype, q.device),
+                 _token_major(h, L, dv_, q.dtype, q.device), _token_major(h, L, dk_, g.dtype, q.device))
+        dq, dk, dv, dg = shard.bwd_output(q, k, v, g, d_out, ctx.prev, ds_next, grads=grads)
         ctx.shard = None
         return dq, dk, dv, dg, None, None, None
+
+
+def _token_major(h, L, d, dtype, device):
+    """[h, L, d] view over [L, h, d] storage."""
+    return torch.empty((L, h, d), dtype=dtype, device=device).transpose(0, 1)
 
 
 def zeco_gla(q, k, v, g, chunk_len=64, comm=None, num_blocks=4):
@@ -115,11 +129,12 @@ class GatedLinearAttention(nn.Module):
             self.norm.to(device)
 
     def _heads(self, t):
-        """[L, H d] -> head-major [H, L, d] (the kernels' layout, glasp/gla.py:29-30)."""
-        return t.view(t.shape[0], self.H, self.d).transpose(0, 1).contiguous()
+        """[L, H d] -> [H, L, d] VIEW (no copy): the fused kernels read strided head slices in place."""
+        return t.view(t.shape[0], self.H, self.d).transpose(0, 1)
 
     def project(self, x):
-        """x [L, hidden] -> q, k, v [H, L, d] (x dtype), g [H, L, d] fp32 log gates (< 0), r [L, H, d]."""
+        """x [L, hidden] -> q, k, v, g [H, L, d] strided views of token-major buffers (g fp32 log gates < 0),
+        r [L, H, d]."""
         qkvr = torch.matmul(x, self.w_qkvr)
         q, k, v, r = qkvr.split(self.hidden, dim=1)
         z = torch.matmul(torch.matmul(x, self.wg1), self.wg2).float() + self.bg

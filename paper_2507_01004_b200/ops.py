@@ -259,8 +259,24 @@ class ZecoShard:
         return torch.empty((self.geo.h, self.geo.dk, self.geo.dv), dtype=self.geo.acc, device=self.device)
 
     def _chk(self, t, name, width):
-        return _req(t, name, self.geo.acc if name in ("g", "s_prev", "ds_next") else self.geo.dtype,
-                    (self.geo.h, self.geo.L, width) if width else (self.geo.h, self.geo.dk, self.geo.dv))
+        """Validate one operand.  Per-rank [h, L, width] tensors may be strided views (channels contiguous,
+        e.g. head slices of a token-major [L, h * width] buffer) on the fused path; the SIMT path gets
+        dense copies."""
+        if width == 0:
+            return _req(t, name, self.geo.acc, (self.geo.h, self.geo.dk, self.geo.dv))
+        dt = self.geo.acc if name in ("g", "dg") else self.geo.dtype
+        shape = (self.geo.h, self.geo.L, width)
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise DimsError(f"{name} must be a CUDA torch tensor")
+        if tuple(t.shape) != shape or t.dtype != dt:
+            raise DimsError(f"{name}: expected {dt} {shape}, got {t.dtype} {tuple(t.shape)}")
+        if not self.fast or t.stride(2) != 1:
+            t = t.contiguous()
+        return t
+
+    @staticmethod
+    def _ref(t):
+        return _native.Tensor(t.data_ptr(), t.stride(1), t.stride(0))
 
     def fwd_local(self, k, v, g):
         """local scan -> (S_local_final [h,dk,dv], G_tot [h,dk])."""
@@ -268,30 +284,35 @@ class ZecoShard:
         k, v, g = self._chk(k, "k", geo.dk), self._chk(v, "v", geo.dv), self._chk(g, "g", geo.dk)
         s_local = self._state()
         g_tot = torch.empty((geo.h, geo.dk), dtype=geo.acc, device=self.device)
-        _native.call("zgla_zeco_fwd_local", ctypes.byref(self.shape), self.sms, _p(k), _p(v), _p(g), _p(self.ws),
-                     _p(s_local), _p(g_tot), _stream())
+        _native.call("zgla_zeco_fwd_local_v", ctypes.byref(self.shape), self.sms, self._ref(k), self._ref(v),
+                     self._ref(g), _p(self.ws), _p(s_local), _p(g_tot), _stream())
         return s_local, g_tot
 
     def fwd_output(self, q, k, v, g, s_prev=None, out=None):
+        """outputs [h, L, dv]; ``out`` may be a strided view (e.g. of a token-major [L, h * dv] buffer)."""
         geo = self.geo
         q, k, v, g = (self._chk(q, "q", geo.dk), self._chk(k, "k", geo.dk), self._chk(v, "v", geo.dv),
                       self._chk(g, "g", geo.dk))
         if s_prev is not None:
             s_prev = self._chk(s_prev, "s_prev", 0)
         o = out if out is not None else torch.empty((geo.h, geo.L, geo.dv), dtype=geo.dtype, device=self.device)
-        _native.call("zgla_zeco_fwd_output", ctypes.byref(self.shape), self.sms, _p(q), _p(k), _p(v), _p(g),
-                     _p(self.ws), _p(s_prev), _p(o), _stream())
+        o_use = self._chk(o, "o", geo.dv)
+        _native.call("zgla_zeco_fwd_output_v", ctypes.byref(self.shape), self.sms, self._ref(q), self._ref(k),
+                     self._ref(v), self._ref(g), _p(self.ws), _p(s_prev), self._ref(o_use), _stream())
+        if o_use.data_ptr() != o.data_ptr():
+            o.copy_(o_use)
         return o
 
     def bwd_local(self, q, g, d_out):
         geo = self.geo
         q, g, d_out = self._chk(q, "q", geo.dk), self._chk(g, "g", geo.dk), self._chk(d_out, "d_out", geo.dv)
         ds0 = self._state()
-        _native.call("zgla_zeco_bwd_local", ctypes.byref(self.shape), self.sms, _p(q), _p(g), _p(d_out),
-                     _p(self.ws), _p(ds0), _stream())
+        _native.call("zgla_zeco_bwd_local_v", ctypes.byref(self.shape), self.sms, self._ref(q), self._ref(g),
+                     self._ref(d_out), _p(self.ws), _p(ds0), _stream())
         return ds0
 
     def bwd_output(self, q, k, v, g, d_out, s_prev=None, ds_next=None, grads=None):
+        """(dq, dk, dv, dg) [h, L, .]; ``grads`` may be strided views."""
         geo = self.geo
         q, k, v, g = (self._chk(q, "q", geo.dk), self._chk(k, "k", geo.dk), self._chk(v, "v", geo.dv),
                       self._chk(g, "g", geo.dk))
@@ -301,11 +322,17 @@ class ZecoShard:
         if ds_next is not None:
             ds_next = self._chk(ds_next, "ds_next", 0)
         if grads is None:
-            grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty_like(g))
-        dq, dk, dv, dg = grads
-        _native.call("zgla_zeco_bwd_output", ctypes.byref(self.shape), self.sms, _p(q), _p(k), _p(v), _p(g),
-                     _p(d_out), _p(self.ws), _p(s_prev), _p(ds_next), _p(dq), _p(dk), _p(dv), _p(dg), _stream())
-        return dq, dk, dv, dg
+            grads = tuple(torch.empty((geo.h, geo.L, w), dtype=dt, device=self.device)
+                          for w, dt in ((geo.dk, geo.dtype), (geo.dk, geo.dtype), (geo.dv, geo.dtype),
+                                        (geo.dk, geo.acc)))
+        use = [self._chk(x, n, w) for x, n, w in zip(grads, ("dq", "dk", "dv", "dg"), (geo.dk, geo.dk, geo.dv, geo.dk))]
+        _native.call("zgla_zeco_bwd_output_v", ctypes.byref(self.shape), self.sms, self._ref(q), self._ref(k),
+                     self._ref(v), self._ref(g), self._ref(d_out), _p(self.ws), _p(s_prev), _p(ds_next),
+                     *(self._ref(x) for x in use), _stream())
+        for x, u in zip(grads, use):
+            if u.data_ptr() != x.data_ptr():
+                x.copy_(u)
+        return tuple(grads)
 
 
 # ---------------------------------------------------------------- All-Scan, list form

@@ -172,3 +172,40 @@ def test_fast_strong_decay_inside_domain(lo, hi):
     for key in ("o", "dq", "dk", "dv", "dg"):
         assert np.all(np.isfinite(got[key])), key
     check(got, oracle(q, k, v, g, do, P))
+
+
+def test_fast_strided_views_bitwise():
+    """zgla_tensor strides: q/k/v/g/dO as head slices of token-major buffers and o/dq/dk/dv/dg written
+    into token-major buffers give bitwise the same results as dense [h, L, d] tensors."""
+    from paper_2507_01004_b200 import ops
+    torch.manual_seed(3)
+    h, L, D = 3, 1024, 128
+    dense = [(torch.rand(h, L, D, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+    g = torch.rand(h, L, D, device="cuda") * (math.log(0.999) - math.log(0.9)) + math.log(0.9)
+    do = (torch.rand(h, L, D, device="cuda") * 2 - 1).to(torch.bfloat16)
+
+    def token_major(x, pad=0):  # [L, h * D + pad] storage, [h, L, D] view
+        buf = torch.zeros(L, h * D + pad, dtype=x.dtype, device="cuda")
+        view = buf[:, :h * D].view(L, h, D).transpose(0, 1)
+        view.copy_(x)
+        return view
+
+    def run(q, k, v, g, do, outs):
+        sh = ops.ZecoShard(h, L, D, D, 64, torch.bfloat16)
+        sh.fwd_local(k, v, g)
+        o = sh.fwd_output(q, k, v, g, out=outs[0])
+        sh.bwd_local(q, g, do)
+        grads = sh.bwd_output(q, k, v, g, do, grads=outs[1:])
+        torch.cuda.synchronize()
+        return [o] + list(grads)
+
+    outs_d = [torch.empty(h, L, D, dtype=torch.bfloat16, device="cuda") for _ in range(4)] + \
+             [torch.empty(h, L, D, device="cuda")]
+    a = run(*dense, g, do, outs_d)
+    strided_in = [token_major(x, pad=64) for x in dense] + [token_major(g, pad=32), token_major(do)]
+    outs_s = [token_major(torch.empty(h, L, D, dtype=torch.bfloat16, device="cuda")) for _ in range(4)] + \
+             [token_major(torch.empty(h, L, D, device="cuda"), pad=16)]
+    b = run(*strided_in, outs_s)
+    for name, x, y in zip(("o", "dq", "dk", "dv", "dg"), a, b):
+        assert y.stride(2) == 1 and y.stride(0) != L * D  # really strided
+        assert torch.equal(x, y), name
