@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_do);
       tma_prefetch_desc(&tm_sp);
+      const uint64_t pol = ZGLA_CONSUMER_EVICT_FIRST ? l2_policy_evict_first() : l2_policy_evict_normal();
       for (int m = 0; m < nt; ++m) {
         const int st = m % BO_NS, ph = (m / BO_NS) & 1;
         const int n = t1 - 1 - m;
@@ -144,14 +145,14 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], BO_STAGE);
         const int r = n * T;
-        tile_load<DENSE>(sb, &tm_q, &full[st], 0, r, hh, L, in3d);
-        tile_load<DENSE>(sb + PANEL, &tm_q, &full[st], 64, r, hh, L, in3d);
-        tile_load<DENSE>(sb + TILE_BF16, &tm_k, &full[st], 0, r, hh, L, in3d);
-        tile_load<DENSE>(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r, hh, L, in3d);
-        tile_load<DENSE>(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r, hh, L, in3d);
-        tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d);
-        tile_load<DENSE>(sb + 3 * TILE_BF16, &tm_do, &full[st], 0, r, hh, L, in3d);
-        tile_load<DENSE>(sb + 3 * TILE_BF16 + PANEL, &tm_do, &full[st], 64, r, hh, L, in3d);
+        tile_load<DENSE>(sb, &tm_q, &full[st], 0, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + PANEL, &tm_q, &full[st], 64, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + TILE_BF16, &tm_k, &full[st], 0, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + 3 * TILE_BF16, &tm_do, &full[st], 0, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + 3 * TILE_BF16 + PANEL, &tm_do, &full[st], 64, r, hh, L, in3d, pol);
         mbar_wait(sp_empty, (m & 1) ^ 1);
         mbar_arrive_expect_tx(sp_full, STATE_BF16);
         const int rs = (hh * ntiles + n) * D;

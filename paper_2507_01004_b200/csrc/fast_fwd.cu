@@ -77,18 +77,24 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
       tma_prefetch_desc(&tm_a);
       tma_prefetch_desc(&tm_b);
       tma_prefetch_desc(&tm_g);
+      // L2 reuse by the consumer kernel: it walks the segment in the opposite direction, so the tiles read
+      // LAST here are read FIRST there.  The first part of this walk is loaded evict-first so that the
+      // tail of the walk is what stays resident.
+      const uint64_t pol_first = l2_policy_evict_first(), pol_keep = l2_policy_evict_normal();
+      const int keep_from = nt - (nt * ZGLA_L2_KEEP_PCT) / 100;
       for (int j = 0; j < nt; ++j) {
         const int st = j % KS_NS, ph = (j / KS_NS) & 1;
         const int tile = DIR == 0 ? t1 - 1 - j : t0 + j;
+        const uint64_t pol = j >= keep_from ? pol_keep : pol_first;
         uint8_t* sa = smem + st * KS_STAGE;
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], KS_STAGE);
         const int r = tile * T;
-        tile_load<DENSE>(sa, &tm_a, &full[st], 0, r, hh, L, in3d);
-        tile_load<DENSE>(sa + PANEL, &tm_a, &full[st], 64, r, hh, L, in3d);
-        tile_load<DENSE>(sa + TILE_BF16, &tm_b, &full[st], 0, r, hh, L, in3d);
-        tile_load<DENSE>(sa + TILE_BF16 + PANEL, &tm_b, &full[st], 64, r, hh, L, in3d);
-        tile_load<DENSE>(sa + 2 * TILE_BF16, &tm_g, &full[st], 0, r, hh, L, in3d);
+        tile_load<DENSE>(sa, &tm_a, &full[st], 0, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sa + PANEL, &tm_a, &full[st], 64, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sa + TILE_BF16, &tm_b, &full[st], 0, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sa + TILE_BF16 + PANEL, &tm_b, &full[st], 64, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sa + 2 * TILE_BF16, &tm_g, &full[st], 0, r, hh, L, in3d, pol);
       }
     }
   } else if (warp == 9) {
@@ -336,18 +342,19 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_g);
+      const uint64_t pol = ZGLA_CONSUMER_EVICT_FIRST ? l2_policy_evict_first() : l2_policy_evict_normal();
       for (int n = 0; n < nt; ++n) {
         const int st = n % FO_NS, ph = (n / FO_NS) & 1;
         uint8_t* sb = smem + st * FO_STAGE;
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], FO_STAGE);
         const int r = (t0 + n) * T;
-        tile_load<DENSE>(sb, &tm_q, &full[st], 0, r, hh, L, in3d);
-        tile_load<DENSE>(sb + PANEL, &tm_q, &full[st], 64, r, hh, L, in3d);
-        tile_load<DENSE>(sb + TILE_BF16, &tm_k, &full[st], 0, r, hh, L, in3d);
-        tile_load<DENSE>(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r, hh, L, in3d);
-        tile_load<DENSE>(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r, hh, L, in3d);
-        tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d);
+        tile_load<DENSE>(sb, &tm_q, &full[st], 0, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + PANEL, &tm_q, &full[st], 64, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + TILE_BF16, &tm_k, &full[st], 0, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r, hh, L, in3d, pol);
+        tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d, pol);
         ZTRACE(tr, 0, n);
       }
     }
