@@ -26,35 +26,38 @@ from dataclasses import dataclass
 
 from .cluster import NetConfig
 from .errors import ConfigError
+from .gla import ModelDims
 
 METHODS = ("ulysses", "megatron_cp", "lasp1", "lasp2", "zeco")
+SIMULATED_METHODS = ("zeco", "lasp1", "lasp2")
 TABLE_COLUMNS = ("method", "P", "L", "D", "e", "N", "volume_elements", "compute_ops", "t_model_seconds")
 
 
 @dataclass(frozen=True)
 class CostParams:
-    """Inputs of the closed forms (glasp/costmodel.py:38-62); dims: heads, key_dim, value_dim."""
+    """Inputs of the closed forms, same fields as glasp/costmodel.py:38-62 (dims: ModelDims)."""
 
     net: NetConfig
-    heads: int
-    key_dim: int
-    value_dim: int
+    dims: ModelDims
     num_ranks: int
     pipeline_blocks: int = 1
+    per_chunk_compute: float = 0.0
     chunks_per_rank: int = 1
     tokens_per_rank: int = 1
 
     def __post_init__(self):
-        if self.num_ranks < 1 or self.pipeline_blocks < 1:
-            raise ConfigError("num_ranks and pipeline_blocks must be >= 1")
+        if self.num_ranks < 1:
+            raise ConfigError(f"num_ranks must be >= 1, got {self.num_ranks}")
+        if self.pipeline_blocks < 1:
+            raise ConfigError(f"pipeline_blocks must be >= 1, got {self.pipeline_blocks}")
         if self.chunks_per_rank < 1 or self.tokens_per_rank < 1:
             raise ConfigError("chunks_per_rank and tokens_per_rank must be positive")
-        if min(self.heads, self.key_dim, self.value_dim) < 1:
-            raise ConfigError("dims must be positive")
+        if self.per_chunk_compute < 0.0:
+            raise ConfigError("per_chunk_compute must be >= 0")
 
     @property
     def state_elements(self) -> int:
-        return self.heads * self.key_dim * self.value_dim
+        return self.dims.state_elements
 
 
 @dataclass(frozen=True)
@@ -75,20 +78,20 @@ def tau(size: float, net: NetConfig) -> float:
 
 def t_allscan(p: CostParams) -> float:
     """Eq. 13: (K + P - 1) tau(S / K); a single rank sends nothing."""
-    if p.key_dim % p.pipeline_blocks:
-        raise ConfigError(f"pipeline_blocks {p.pipeline_blocks} does not divide key dim {p.key_dim}")
+    if p.dims.key_dim % p.pipeline_blocks:
+        raise ConfigError(f"pipeline_blocks {p.pipeline_blocks} does not divide key dim {p.dims.key_dim}")
     if p.num_ranks == 1:
         return 0.0
     hops = p.pipeline_blocks + p.num_ranks - 1
     return hops * tau(p.state_elements / p.pipeline_blocks, p.net)
 
 
-def volume_compute(method: str, p: CostParams):
+def volume_compute_table(method: str, p: CostParams):
     """(communication elements, compute ops) per method, D = h * e (square per-head states)."""
-    if p.key_dim != p.value_dim:
+    if p.dims.key_dim != p.dims.value_dim:
         raise ConfigError("the unified table assumes e_k == e_v")
-    e, P, L, N = p.key_dim, p.num_ranks, p.tokens_per_rank, p.chunks_per_rank
-    D = p.heads * e
+    e, P, L, N = p.dims.key_dim, p.num_ranks, p.tokens_per_rank, p.chunks_per_rank
+    D = p.dims.heads * e
     table = {
         "ulysses": (4 * L * D, L * L * D * P),
         "megatron_cp": (2 * P * L * D, L * L * D * P),
@@ -108,19 +111,26 @@ def t_strategies(p: CostParams, t_ideal: float, t_overlap: float) -> CostReport:
         raise ConfigError(f"t_overlap {t_overlap} exceeds t_ideal {t_ideal}")
     ts = tau(p.state_elements, p.net)
     P = p.num_ranks
-    vc = {m: volume_compute(m, p) for m in METHODS}
+    vc = {m: volume_compute_table(m, p) for m in METHODS}
     return CostReport(t_allscan=t_allscan(p), t_zeco=t_ideal - t_overlap + ts, t_lasp1=P * (t_ideal + ts),
                       t_lasp2=t_ideal + P * ts, volumes={m: v[0] for m, v in vc.items()},
                       computes={m: v[1] for m, v in vc.items()})
+
+
+def table_note(method: str) -> str:
+    """Caveat attached to a table row (glasp/costmodel.py:140-148)."""
+    return {"lasp1": "volume counts serialized order; per-rank physical volume is D*e",
+            "lasp2": "table volume P*D*e vs per-rank gather volume (P-1)*D*e",
+            "zeco": "compute term N*d read with d = D"}.get(method, "")
 
 
 def table_rows(p: CostParams, methods=METHODS, report: CostReport | None = None):
     times = {} if report is None else {"zeco": report.t_zeco, "lasp1": report.t_lasp1, "lasp2": report.t_lasp2}
     rows = []
     for m in methods:
-        vol, comp = volume_compute(m, p)
-        rows.append({"method": m, "P": p.num_ranks, "L": p.tokens_per_rank, "D": p.heads * p.key_dim,
-                     "e": p.key_dim, "N": p.chunks_per_rank, "volume_elements": vol, "compute_ops": comp,
+        vol, comp = volume_compute_table(m, p)
+        rows.append({"method": m, "P": p.num_ranks, "L": p.tokens_per_rank, "D": p.dims.heads * p.dims.key_dim,
+                     "e": p.dims.key_dim, "N": p.chunks_per_rank, "volume_elements": vol, "compute_ops": comp,
                      "t_model_seconds": times.get(m, "")})
     return rows
 

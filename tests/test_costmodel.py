@@ -10,12 +10,13 @@ import pytest
 from paper_2507_01004_b200 import costmodel as cm
 from paper_2507_01004_b200.cluster import NetConfig
 from paper_2507_01004_b200.errors import ConfigError
+from paper_2507_01004_b200.gla import ModelDims
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _p(P=8, K=16, net=NetConfig(1e-6, 1e9, 4)):
-    return cm.CostParams(net=net, heads=16, key_dim=128, value_dim=128, num_ranks=P, pipeline_blocks=K,
+    return cm.CostParams(net=net, dims=ModelDims(16, 128, 128), num_ranks=P, pipeline_blocks=K,
                          chunks_per_rank=256, tokens_per_rank=16384)
 
 
@@ -67,5 +68,7 @@ def test_closed_forms_match_reference():
         a, b = cm.t_strategies(ours, 2.0, 0.5), ref.t_strategies(theirs, 2.0, 0.5)
         assert (a.t_zeco, a.t_lasp1, a.t_lasp2) == (b.t_zeco, b.t_lasp1, b.t_lasp2)
         for m in cm.METHODS:
-            assert cm.volume_compute(m, ours) == ref.volume_compute_table(m, theirs)
+            assert cm.volume_compute_table(m, ours) == ref.volume_compute_table(m, theirs)
         assert [{k: r[k] for k in cm.TABLE_COLUMNS} for r in cm.table_rows(ours)] == ref.table_rows(theirs)
+        assert all(cm.table_note(m) == ref.table_note(m) for m in cm.METHODS)
+    assert cm.SIMULATED_METHODS == ref.SIMULATED_METHODS and cm.TABLE_COLUMNS == ref.TABLE_COLUMNS
