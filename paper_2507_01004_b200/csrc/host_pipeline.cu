@@ -56,6 +56,25 @@ static int get_ctx(Ctx** out, size_t nev) {
   return ZGLA_OK;
 }
 
+// the five transfers of one group and direction: one batched submission (ZGLA_COPY_BATCH=0: five copies)
+static int copy5(void** dsts, void** srcs, size_t* sizes, cudaMemcpyKind kind, cudaStream_t st) {
+  static const bool batch = [] {
+    const char* e = std::getenv("ZGLA_COPY_BATCH");
+    return !(e && e[0] == '0');
+  }();
+  if (batch) {
+    cudaMemcpyAttributes attr = {};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t idx = 0, fail = 0;
+    if (cudaMemcpyBatchAsync(dsts, srcs, sizes, 5, &attr, &idx, 1, &fail, st) == cudaSuccess) return ZGLA_OK;
+    cudaGetLastError();  // fall back to individual copies
+  }
+  for (int i = 0; i < 5; ++i)
+    if (cudaError_t r = cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], kind, st)) return cuda_fail(r, "host copy");
+  return ZGLA_OK;
+}
+
 inline long long al256(long long x) { return (x + 255) & ~255ll; }
 inline int esize(int dt) { return dt == ZGLA_BF16 ? 2 : dt == ZGLA_F32 ? 4 : 8; }
 inline int asize(int dt) { return dt == ZGLA_F64 ? 8 : 4; }
@@ -193,11 +212,16 @@ extern "C" int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head
     const int h0 = gb[j], h1 = gb[j + 1];
     const int hg = h1 - h0;
     if (chain) cudaStreamWaitEvent(cx->h2d, ev_comp[j], 0);  // previous call's kernels of group j
-    for (int i = 0; i < 5; ++i) {
-      if (cudaError_t r = cudaMemcpyAsync(base + lo.in[i] + h0 * ph_in[i],
-                                          reinterpret_cast<const unsigned char*>(hin[i]) + h0 * ph_in[i],
-                                          hg * ph_in[i], cudaMemcpyHostToDevice, cx->h2d))
-        return cuda_fail(r, "zgla_zeco_fwd_bwd_host h2d");
+    {
+      void* dsts[5];
+      void* srcs[5];
+      size_t sizes[5];
+      for (int i = 0; i < 5; ++i) {
+        dsts[i] = base + lo.in[i] + h0 * ph_in[i];
+        srcs[i] = const_cast<unsigned char*>(reinterpret_cast<const unsigned char*>(hin[i])) + h0 * ph_in[i];
+        sizes[i] = (size_t)(hg * ph_in[i]);
+      }
+      if (int rc = copy5(dsts, srcs, sizes, cudaMemcpyHostToDevice, cx->h2d)) return rc;
     }
     cudaEventRecord(ev_in[j], cx->h2d);
     if (trace) cudaEventRecord(tev[3 * j], cx->h2d);
@@ -236,11 +260,16 @@ extern "C" int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head
     cudaEventRecord(ev_comp[j], st);
     if (trace) cudaEventRecord(tev[3 * j + 1], st);
     cudaStreamWaitEvent(cx->d2h, ev_comp[j], 0);
-    for (int i = 0; i < 5; ++i) {
-      if (cudaError_t r = cudaMemcpyAsync(reinterpret_cast<unsigned char*>(hout[i]) + h0 * ph_out[i],
-                                          base + lo.out[i] + h0 * ph_out[i], hg * ph_out[i],
-                                          cudaMemcpyDeviceToHost, cx->d2h))
-        return cuda_fail(r, "zgla_zeco_fwd_bwd_host d2h");
+    {
+      void* dsts[5];
+      void* srcs[5];
+      size_t sizes[5];
+      for (int i = 0; i < 5; ++i) {
+        dsts[i] = reinterpret_cast<unsigned char*>(hout[i]) + h0 * ph_out[i];
+        srcs[i] = base + lo.out[i] + h0 * ph_out[i];
+        sizes[i] = (size_t)(hg * ph_out[i]);
+      }
+      if (int rc = copy5(dsts, srcs, sizes, cudaMemcpyDeviceToHost, cx->d2h)) return rc;
     }
     cudaEventRecord(ev_d2h[j], cx->d2h);
     if (trace) cudaEventRecord(tev[3 * j + 2], cx->d2h);
