@@ -17,7 +17,8 @@
  * Precision modes (zgla_dtype):
  *   ZGLA_BF16: q,k,v,dO,o,dq,dk,dv are bf16; g, dg, states are fp32.  ZeCO
  *              entry points use the tcgen05/TMEM/TMA kernels when
- *              dk,dv in {64,128} and L % 64 == 0.
+ *              dk == dv in {64, 128} and L % 64 == 0 (d = 64 runs the 128-channel
+ *              kernels on TMA zero-filled channels).
  *   ZGLA_F32 : everything fp32 ("fp32 validation mode", SIMT FMA kernels).
  *   ZGLA_F64 : everything fp64 (bit-for-bit reference semantics for tests).
  */

@@ -94,7 +94,7 @@ static int check_refs(const zgla_shape* s, std::initializer_list<const zgla_tens
   for (const zgla_tensor* t : ts) {
     if (!t || !t->data) return ZGLA_ERR_DIMS;
     if (fast_path) {
-      if (!fast::ref_ok(fast::as_ref(t, s->seq_len, s->heads), 2)) {
+      if (!fast::ref_ok(fast::as_ref(t, s->seq_len, s->heads, s->key_dim), 2)) {
         set_error("strided tensor: base and strides must be 16-byte aligned, token stride >= channels");
         return ZGLA_ERR_LAYOUT;
       }
@@ -114,7 +114,7 @@ extern "C" int zgla_zeco_fwd_local_v(const zgla_shape* s, int num_sms, const zgl
   cudaStream_t st = (cudaStream_t)stream;
   const long long L = s->seq_len;
   if (fp)
-    return fast_fwd_local(s, num_sms, fast::as_ref(k, L, s->heads), fast::as_ref(v, L, s->heads), fast::as_ref(g, L, s->heads), ws, s_local, g_tot,
+    return fast_fwd_local(s, num_sms, fast::as_ref(k, L, s->heads, s->key_dim), fast::as_ref(v, L, s->heads, s->key_dim), fast::as_ref(g, L, s->heads, s->key_dim), ws, s_local, g_tot,
                           st);
   return generic_zeco_fwd_local(s, k->data, v->data, g->data, ws, s_local, g_tot, st);
 }
@@ -128,8 +128,8 @@ extern "C" int zgla_zeco_fwd_output_v(const zgla_shape* s, int num_sms, const zg
   cudaStream_t st = (cudaStream_t)stream;
   const long long L = s->seq_len;
   if (fp)
-    return fast_fwd_output(s, num_sms, fast::as_ref(q, L, s->heads), fast::as_ref(k, L, s->heads), fast::as_ref(v, L, s->heads),
-                           fast::as_ref(g, L, s->heads), ws, s_prev, fast::as_ref(o, L, s->heads), st);
+    return fast_fwd_output(s, num_sms, fast::as_ref(q, L, s->heads, s->key_dim), fast::as_ref(k, L, s->heads, s->key_dim), fast::as_ref(v, L, s->heads, s->key_dim),
+                           fast::as_ref(g, L, s->heads, s->key_dim), ws, s_prev, fast::as_ref(o, L, s->heads, s->key_dim), st);
   return generic_zeco_fwd_output(s, q->data, k->data, v->data, g->data, ws, s_prev, o->data, st);
 }
 
@@ -141,7 +141,7 @@ extern "C" int zgla_zeco_bwd_local_v(const zgla_shape* s, int num_sms, const zgl
   cudaStream_t st = (cudaStream_t)stream;
   const long long L = s->seq_len;
   if (fp)
-    return fast_bwd_local(s, num_sms, fast::as_ref(q, L, s->heads), fast::as_ref(g, L, s->heads), fast::as_ref(d_out, L, s->heads), ws, ds_local0,
+    return fast_bwd_local(s, num_sms, fast::as_ref(q, L, s->heads, s->key_dim), fast::as_ref(g, L, s->heads, s->key_dim), fast::as_ref(d_out, L, s->heads, s->key_dim), ws, ds_local0,
                           st);
   return generic_zeco_bwd_local(s, q->data, g->data, d_out->data, ws, ds_local0, st);
 }
@@ -157,9 +157,9 @@ extern "C" int zgla_zeco_bwd_output_v(const zgla_shape* s, int num_sms, const zg
   cudaStream_t st = (cudaStream_t)stream;
   const long long L = s->seq_len;
   if (fp)
-    return fast_bwd_output(s, num_sms, fast::as_ref(q, L, s->heads), fast::as_ref(k, L, s->heads), fast::as_ref(v, L, s->heads),
-                           fast::as_ref(g, L, s->heads), fast::as_ref(d_out, L, s->heads), ws, s_prev, ds_next, fast::as_ref(dq, L, s->heads),
-                           fast::as_ref(dk, L, s->heads), fast::as_ref(dv, L, s->heads), fast::as_ref(dg, L, s->heads), st);
+    return fast_bwd_output(s, num_sms, fast::as_ref(q, L, s->heads, s->key_dim), fast::as_ref(k, L, s->heads, s->key_dim), fast::as_ref(v, L, s->heads, s->key_dim),
+                           fast::as_ref(g, L, s->heads, s->key_dim), fast::as_ref(d_out, L, s->heads, s->key_dim), ws, s_prev, ds_next, fast::as_ref(dq, L, s->heads, s->key_dim),
+                           fast::as_ref(dk, L, s->heads, s->key_dim), fast::as_ref(dv, L, s->heads, s->key_dim), fast::as_ref(dg, L, s->heads, s->key_dim), st);
   return generic_zeco_bwd_output(s, q->data, k->data, v->data, g->data, d_out->data, ws, s_prev, ds_next, dq->data,
                                  dk->data, dv->data, dg->data, st);
 }

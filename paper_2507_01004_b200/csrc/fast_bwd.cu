@@ -49,7 +49,8 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
     bwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                    const __grid_constant__ CUtensorMap tm_sp, const __grid_constant__ CUtensorMap tm_g,
-                   const float* __restrict__ g, long long gts, long long ghs, long long L, int in3d, int nseg,
+                   const float* __restrict__ g, long long gts, long long ghs, long long L, int in3d, int dr,
+                   int nseg,
                    int ntiles, const float* __restrict__ Sin, const float* __restrict__ cumG,
                    const float* __restrict__ dS, const float* __restrict__ gamseg, const float* __restrict__ s_prev,
                    const float* __restrict__ Dend, const float* __restrict__ cumGr,
@@ -243,10 +244,13 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
 #pragma unroll
       if constexpr (DENSE) {
         for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);  // immediate offsets
-      } else {
+      } else if (c < dr) {
         const float* pr = gp;  // runtime stride: one pointer bump per row keeps the loads back to back
 #pragma unroll
         for (int r = 0; r < 64; ++r, pr += gts) lb[r] = __ldg(pr);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 64; ++r) lb[r] = 0.f;  // zero-filled channel of a d = 64 head
       }
 #pragma unroll
       for (int r = 1; r < 64; ++r) lb[r] += lb[r - 1];
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const float cgr = ds_next ? expf(cumGr[(hh * nseg + s) * D + c]) : 0.f;
       const float cg = s_prev ? expf(cumG[(hh * nseg + s) * D + c]) : 0.f;
       const float eg = expf(gamseg[(hh * nseg + s) * D + c]);
-      const long long pidx = ((long long)hh * D + c) * D + 64 * ch;
+      const long long pidx = ((long long)hh * dr + c) * dr + 64 * ch;  // API states are [h][dr][dr]
       float rho = 0.f;
 #pragma unroll 1
       for (int hf = 0; hf < 2; ++hf) {
@@ -315,11 +319,12 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           float4 dd = make_float4(Dend[o], Dend[o + D], Dend[o + 2 * D], Dend[o + 3 * D]);
           float4 si = make_float4(Sin[o], Sin[o + D], Sin[o + 2 * D], Sin[o + 3 * D]);
           const float4 ds = make_float4(dS[o], dS[o + D], dS[o + 2 * D], dS[o + 3 * D]);
-          if (ds_next) {
+          const bool inb = c < dr && 64 * ch + jj < dr;
+          if (ds_next && inb) {
             const float4 a = *reinterpret_cast<const float4*>(ds_next + pidx + jj);
             dd.x += cgr * a.x; dd.y += cgr * a.y; dd.z += cgr * a.z; dd.w += cgr * a.w;
           }
-          if (s_prev) {
+          if (s_prev && inb) {
             const float4 a = *reinterpret_cast<const float4*>(s_prev + pidx + jj);
             si.x += cg * a.x; si.y += cg * a.y; si.z += cg * a.z; si.w += cg * a.w;
           }
@@ -440,14 +445,12 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           const float dlt = __uint_as_float(dl[u]) * LOG2E;
           da[i] = qh[u] * q_raw - kh[u] * k_raw;
           tsum += da[i];
-#ifndef ZGLA_EXP_NOSTORE
-          *pdq = __float2bfloat16_rn(q_raw * fast_exp2(dlt));
-          *pdk = __float2bfloat16_rn(k_raw * fast_exp2(-dlt));
-          *pdv = __float2bfloat16_rn(__uint_as_float(gv8[u]));
+          if (DENSE || c < dr) {  // channels of a d = 64 head beyond 64 are padding
+            *pdq = __float2bfloat16_rn(q_raw * fast_exp2(dlt));
+            *pdk = __float2bfloat16_rn(k_raw * fast_exp2(-dlt));
+            *pdv = __float2bfloat16_rn(__uint_as_float(gv8[u]));
+          }
           pdq += gs.qt, pdk += gs.kt, pdv += gs.vt;
-#else
-          if (q_raw * fast_exp2(dlt) + k_raw * fast_exp2(-dlt) + __uint_as_float(gv8[u]) == 1234.5f) dq[0] = 0;
-#endif
         }
       }
       tc_fence_before();
@@ -462,11 +465,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       float* pdg = dg + hh * gs.gh + tok0 * gs.gt + c;
 #pragma unroll
       for (int i = 0; i < 32; ++i, pdg += gs.gt) {
-#ifndef ZGLA_EXP_NOSTORE
-        *pdg = base;
-#else
-        if (base == 1234.5f) dg[0] = 0;
-#endif
+        if (DENSE || c < dr) *pdg = base;
         base -= da[i];
       }
       if (tid == 0) ZTRACE(tr, 9, m);
@@ -504,7 +503,7 @@ int fast_bwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   auto kern = dn ? bwd_out_kernel<true> : bwd_out_kernel<false>;
   set_smem_once((const void*)kern, (int)BO_SMEM);
   if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp, mg,
-                                (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, pl.nseg, pl.ntiles,
+                                (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
                                 (const float*)w.Sin, (const float*)w.cumG, (const float*)w.dS, (const float*)w.gam, (const float*)s_prev,
                                 (const float*)w.Dend, (const float*)w.cumGr, (const float*)ds_next,
                                 (__nv_bfloat16*)dq.p, (__nv_bfloat16*)dk.p, (__nv_bfloat16*)dv.p, (float*)dg.p, gs,

@@ -140,22 +140,23 @@ struct TRef {
   const void* p;
   long long ts;  // token stride
   long long hs;  // head stride
+  int dr;        // channels actually stored (128, or 64: the kernels see 128 with the rest zero-filled)
 };
 // token / head strides of the four gradient outputs of the backward kernel (elements)
 struct Strides4 {  // token strides fit in 32 bits (fewer live registers in the epilogue); head strides not
   int qt, kt, vt, gt;
   long long qh, kh, vh, gh;
 };
-inline TRef dense_ref(const void* p, long long L) { return TRef{p, D, L * D}; }
-inline TRef as_ref(const zgla_tensor* t, long long L, int heads) {
+inline TRef dense_ref(const void* p, long long L) { return TRef{p, D, L * D, D}; }
+inline TRef as_ref(const zgla_tensor* t, long long L, int heads, int dr) {
   // a single head's head stride is irrelevant: normalise it so dense single-head views stay dense
-  return TRef{t->data, t->token_stride ? t->token_stride : D,
-              (t->head_stride && heads > 1) ? t->head_stride : L * D};
+  return TRef{t->data, t->token_stride ? t->token_stride : dr,
+              (t->head_stride && heads > 1) ? t->head_stride : L * dr, dr};
 }
 // TMA needs 16-byte aligned bases and strides; channel rows are 16-byte vectors for the stores
 inline bool ref_ok(const TRef& r, int esize) {
   return r.p && (reinterpret_cast<uintptr_t>(r.p) & 15) == 0 && (r.ts * esize) % 16 == 0 &&
-         (r.hs * esize) % 16 == 0 && r.ts >= D && r.ts < (1ll << 31) && r.hs >= 0;
+         (r.hs * esize) % 16 == 0 && r.ts >= r.dr && r.ts < (1ll << 31) && r.hs >= 0;
 }
 
 // 3-D map (channels, tokens, heads) over a strided [heads][tokens][D] tensor; box = box_cols x box_rows x 1
@@ -167,8 +168,9 @@ inline int make_map3(CUtensorMap* m, const TRef& r, bool bf16, long long L, int 
     return ZGLA_ERR_CUDA;
   }
   const unsigned eb = bf16 ? 2 : 4;
-  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)L, (cuuint64_t)heads};
-  cuuint64_t strides[2] = {(cuuint64_t)(r.ts * eb), (cuuint64_t)((r.hs ? r.hs : L * D) * eb)};
+  // channels beyond r.dr are outside the map: TMA zero-fills them (d = 64 heads run the d = 128 kernels)
+  cuuint64_t dims[3] = {(cuuint64_t)r.dr, (cuuint64_t)L, (cuuint64_t)heads};
+  cuuint64_t strides[2] = {(cuuint64_t)(r.ts * eb), (cuuint64_t)((r.hs ? r.hs : L * r.dr) * eb)};
   cuuint32_t box[3] = {box_cols, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult e = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
@@ -183,7 +185,7 @@ inline int make_map3(CUtensorMap* m, const TRef& r, bool bf16, long long L, int 
   }
   return ZGLA_OK;
 }
-inline bool is_dense(const TRef& r, long long L) { return r.ts == D && r.hs == L * D; }
+inline bool is_dense(const TRef& r, long long L) { return r.dr == D && r.ts == D && r.hs == L * D; }
 inline int map_act(CUtensorMap* m, const TRef& r, long long L, int heads, bool dense) {  // bf16 64x64 SW128
   if (dense) return make_map(m, r.p, true, (unsigned long long)heads * L, D, 64, T, true);
   return make_map3(m, r, true, L, heads, 64, T, true);

@@ -187,9 +187,9 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
 // instead of nseg.
 constexpr int SCAN_B = 8;
 
-__global__ void fwd_scan_kernel(int h, int nseg, const float* __restrict__ dS, const float* __restrict__ gam,
-                                float* __restrict__ Sin, float* __restrict__ cumG, float* __restrict__ s_local,
-                                float* __restrict__ g_tot) {
+__global__ void fwd_scan_kernel(int h, int nseg, int dr, const float* __restrict__ dS,
+                                const float* __restrict__ gam, float* __restrict__ Sin, float* __restrict__ cumG,
+                                float* __restrict__ s_local, float* __restrict__ g_tot) {
   pdl_wait();
   pdl_trigger();
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -216,13 +216,15 @@ __global__ void fwd_scan_kernel(int h, int nseg, const float* __restrict__ dS, c
       }
     }
   }
-  if (s_local) s_local[((long long)hh * D + c) * D + vv] = run;  // API layout: row-major [h][c][v]
-  if (vv == 0 && g_tot) g_tot[hh * D + c] = cm;
+  // API layout: row-major [h][dr][dr] (the padded channels of d = 64 heads are dropped)
+  if (s_local && c < dr && vv < dr) s_local[((long long)hh * dr + c) * dr + vv] = run;
+  if (vv == 0 && g_tot && c < dr) g_tot[hh * dr + c] = cm;
 }
 
 // backward: Dend[s] = sum_{s'>s} e^{gam(s+1..s'-1)} dD[s'];  ds_local0 = Dend[-1] inclusive of all; cumGr
-__global__ void bwd_scan_kernel(int h, int nseg, const float* __restrict__ dD, const float* __restrict__ gam,
-                                float* __restrict__ Dend, float* __restrict__ cumGr, float* __restrict__ ds0) {
+__global__ void bwd_scan_kernel(int h, int nseg, int dr, const float* __restrict__ dD,
+                                const float* __restrict__ gam, float* __restrict__ Dend, float* __restrict__ cumGr,
+                                float* __restrict__ ds0) {
   pdl_wait();
   pdl_trigger();
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -249,7 +251,7 @@ __global__ void bwd_scan_kernel(int h, int nseg, const float* __restrict__ dD, c
       }
     }
   }
-  if (ds0) ds0[((long long)hh * D + c) * D + vv] = run;
+  if (ds0 && c < dr && vv < dr) ds0[((long long)hh * dr + c) * dr + vv] = run;
 }
 
 // ============================================================== K3: forward outputs
@@ -270,7 +272,8 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
     fwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g,
                    const __grid_constant__ CUtensorMap tm_sp, const float* __restrict__ g, long long gts,
-                   long long ghs, long long L, int in3d, int nseg, int ntiles, const float* __restrict__ Sin,
+                   long long ghs, long long L, int in3d, int dr, int nseg, int ntiles,
+                   const float* __restrict__ Sin,
                    const float* __restrict__ cumG, const float* __restrict__ s_prev,
                    __nv_bfloat16* __restrict__ out, long long ots, long long ohs,
                    __nv_bfloat16* __restrict__ sp_save, unsigned long long* trace, int trace_cta) {
@@ -434,10 +437,13 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
 #pragma unroll
       if constexpr (DENSE) {
         for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);  // immediate offsets
-      } else {
+      } else if (c < dr) {
         const float* pr = gp;  // runtime stride: one pointer bump per row keeps the loads back to back
 #pragma unroll
         for (int r = 0; r < 64; ++r, pr += gts) lb[r] = __ldg(pr);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 64; ++r) lb[r] = 0.f;  // zero-filled channel of a d = 64 head
       }
 #pragma unroll
       for (int r = 1; r < 64; ++r) lb[r] += lb[r - 1];
@@ -493,7 +499,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
     {
       const long long sidx = (long long)(hh * nseg + s) * D * D + c;  // column-major workspace state
       const float cg = s_prev ? expf(cumG[(hh * nseg + s) * D + c]) : 0.f;
-      const float* pv = s_prev ? s_prev + ((long long)hh * D + c) * D : nullptr;
+      const float* pv = (s_prev && c < dr) ? s_prev + ((long long)hh * dr + c) * dr : nullptr;
       // all loads first (two batches of 64 values, straight into TMEM); the bf16 copy S' needs the first
       // tile's reference point, so it is written from TMEM once the prep warps have published it
 #pragma unroll 1
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
             const int col = 32 * (q2 + hq) + j;
             float4 a = make_float4(Sin[sidx + col * D], Sin[sidx + (col + 1) * D], Sin[sidx + (col + 2) * D],
                                    Sin[sidx + (col + 3) * D]);
-            if (pv) {
+            if (pv && col < dr) {
               const float4 b = *reinterpret_cast<const float4*>(pv + col);
               a.x += cg * b.x;
               a.y += cg * b.y;
@@ -606,7 +612,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       for (int q = 0; q < 4; ++q) {
         float o[32];
         tmem_ld32(taddr(tbase, 32 * qd, COL_O + 32 * q), o);
-        if ((lane >> 4) == ob) {
+        if ((lane >> 4) == ob && 32 * q < dr) {
           const int i = 16 * qd + (lane & 15);
           uint4* dst = reinterpret_cast<uint4*>(out + hh * ohs + ((long long)(t0 + n) * T + i) * ots + 32 * q);
 #pragma unroll
@@ -637,7 +643,8 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
 using namespace fast;
 
 bool fast_supported(const zgla_shape* s) {
-  return s && s->dtype == ZGLA_BF16 && s->key_dim == D && s->value_dim == D && s->seq_len % T == 0 &&
+  return s && s->dtype == ZGLA_BF16 && s->key_dim == s->value_dim && (s->key_dim == D || s->key_dim == 64) &&
+         s->seq_len % T == 0 &&
          s->heads * s->seq_len < (1ll << 31) && encode_fn() != nullptr;
 }
 
@@ -664,7 +671,7 @@ int fast_fwd_local(const zgla_shape* s, int num_sms, const TRef& k, const TRef& 
   Ws w = carve(pl, ws);
   if (int rc = launch_seg_state(0, pl, k, v, g, w.dS, w.gam, st)) return rc;
   const long long n = (long long)pl.h * D * D;
-  if (cudaError_t e = launch_k(fwd_scan_kernel, (unsigned)((n + 255) / 256), 256, 0, st, pl.h, pl.nseg,
+  if (cudaError_t e = launch_k(fwd_scan_kernel, (unsigned)((n + 255) / 256), 256, 0, st, pl.h, pl.nseg, k.dr,
                                 (const float*)w.dS, (const float*)w.gam, w.Sin, w.cumG, (float*)s_local, (float*)g_tot))
     return cuda_fail(e, "fwd_scan_kernel");
   return zgla_check_launch();
@@ -687,7 +694,7 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   auto kern = dn ? fwd_out_kernel<true> : fwd_out_kernel<false>;
   set_smem_once((const void*)kern, (int)FO_SMEM);
   if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
-                                (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, pl.nseg, pl.ntiles,
+                                (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
                                 (const float*)w.Sin, (const float*)w.cumG, (const float*)s_prev, (__nv_bfloat16*)o.p,
                                 o.ts, o.hs, w.Sp,
                                 g_trace_buf, g_trace_cta))
@@ -701,7 +708,7 @@ int fast_bwd_local(const zgla_shape* s, int num_sms, const TRef& q, const TRef& 
   Ws w = carve(pl, ws);
   if (int rc = launch_seg_state(1, pl, q, d_out, g, w.dD, w.gam, st)) return rc;
   const long long n = (long long)pl.h * D * D;
-  if (cudaError_t e = launch_k(bwd_scan_kernel, (unsigned)((n + 255) / 256), 256, 0, st, pl.h, pl.nseg,
+  if (cudaError_t e = launch_k(bwd_scan_kernel, (unsigned)((n + 255) / 256), 256, 0, st, pl.h, pl.nseg, q.dr,
                                 (const float*)w.dD, (const float*)w.gam, w.Dend, w.cumGr, (float*)ds0))
     return cuda_fail(e, "bwd_scan_kernel");
   return zgla_check_launch();

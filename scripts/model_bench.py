@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--no-recompute", action="store_true")
+    ap.add_argument("--heads", type=int, default=16, help="16 x 128 (default) or 32 x 64 (the paper's GLA-1B heads)")
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -39,7 +40,7 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = GLAConfig(layers=args.layers, recompute=not args.no_recompute)
+    cfg = GLAConfig(layers=args.layers, recompute=not args.no_recompute, heads=args.heads)
     comm = zd.AllScanP2P(cfg.heads, cfg.hidden // cfg.heads, cfg.hidden // cfg.heads) if world > 1 else None
     torch.manual_seed(0)
     model = GLAModel(cfg, comm=comm, device=dev)

@@ -209,3 +209,14 @@ def test_fast_strided_views_bitwise():
     for name, x, y in zip(("o", "dq", "dk", "dv", "dg"), a, b):
         assert y.stride(2) == 1 and y.stride(0) != L * D  # really strided
         assert torch.equal(x, y), name
+
+
+@pytest.mark.parametrize("P,L,h,long_memory", [(1, 1024, 2, False), (2, 512, 4, True), (4, 256, 3, True)])
+def test_fast_d64_heads_against_oracle(P, L, h, long_memory):
+    """d_k = d_v = 64 (the paper's GLA-1B heads, BASELINE config 1) on the fused path: the 128-channel
+    kernels see the missing channels as TMA zero-fill; guarded stores write only the 64 real ones."""
+    q, k, v, g, do = make_case(h, P, L, seed=200 + P + h, long_memory=long_memory, D=64)
+    got = run_fast(q, k, v, g, do, P)
+    want = oracle(q, k, v, g, do, P)
+    check(got, want)
+    assert rel(got["prev"], want["prev"]) <= TOL_BF16
