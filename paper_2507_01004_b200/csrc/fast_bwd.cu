@@ -119,6 +119,10 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
     mbar_init(&lb_empty[1], 256);
     fence_barrier_init();
   }
+  if (dr < D) {  // d = 64: S' tiles fill only the top-left 64 x 64 block of this buffer
+    for (int i = tid; i < STATE_BF16 / 16; i += BO_THREADS) reinterpret_cast<uint4*>(sp_buf)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+  }
   if (warp == 0) {
     tmem_alloc(tmem_slot, 512);
     tmem_relinquish();
@@ -155,10 +159,15 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         tile_load<DENSE>(sb + 3 * TILE_BF16, &tm_do, &full[st], 0, r, hh, L, in3d, pol);
         tile_load<DENSE>(sb + 3 * TILE_BF16 + PANEL, &tm_do, &full[st], 64, r, hh, L, in3d, pol);
         mbar_wait(sp_empty, (m & 1) ^ 1);
-        mbar_arrive_expect_tx(sp_full, STATE_BF16);
-        const int rs = (hh * ntiles + n) * D;
-        tma_load_2d(sp_buf, &tm_sp, sp_full, 0, rs);
-        tma_load_2d(sp_buf + SPANEL, &tm_sp, sp_full, 64, rs);
+        if (dr == D) {
+          mbar_arrive_expect_tx(sp_full, STATE_BF16);
+          const int rs = (hh * ntiles + n) * D;
+          tma_load_2d(sp_buf, &tm_sp, sp_full, 0, rs);
+          tma_load_2d(sp_buf + SPANEL, &tm_sp, sp_full, 64, rs);
+        } else {  // d = 64: the real 64 x 64 block; the rest of the buffer stays zero (cleared at entry)
+          mbar_arrive_expect_tx(sp_full, T * 128);
+          tma_load_2d(sp_buf, &tm_sp, sp_full, 0, (hh * ntiles + n) * 64);
+        }
         ZTRACE(tr, 0, m);
       }
     }
@@ -497,7 +506,7 @@ int fast_bwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   if (int rc = map_act(&mk, k, pl.L, pl.h, din)) return rc;
   if (int rc = map_act(&mv, v, pl.L, pl.h, din)) return rc;
   if (int rc = map_act(&mdo, d_out, pl.L, pl.h, din)) return rc;
-  if (int rc = make_map(&msp, w.Sp, true, (unsigned long long)pl.h * pl.ntiles * D, D, 64, D, true)) return rc;
+  if (int rc = sp_map(&msp, w.Sp, pl, q.dr)) return rc;
   if (int rc = map_gate(&mg, g, pl.L, pl.h, din && is_dense(g, pl.L))) return rc;
   const Strides4 gs{(int)dq.ts, (int)dk.ts, (int)dv.ts, (int)dg.ts, dq.hs, dk.hs, dv.hs, dg.hs};
   auto kern = dn ? bwd_out_kernel<true> : bwd_out_kernel<false>;

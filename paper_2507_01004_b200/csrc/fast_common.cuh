@@ -185,6 +185,12 @@ inline int make_map3(CUtensorMap* m, const TRef& r, bool bf16, long long L, int 
   }
   return ZGLA_OK;
 }
+// saved chunk-start states S' (bf16): [h * NT * 128 rows][128] in two 64-column boxes of 128 rows, or
+// for d = 64 only the real 64 x 64 block per tile ([h * NT * 64 rows][64], one box)
+inline int sp_map(CUtensorMap* m, void* sp, const Plan& pl, int dr) {
+  if (dr == D) return make_map(m, sp, true, (unsigned long long)pl.h * pl.ntiles * D, D, 64, D, true);
+  return make_map(m, sp, true, (unsigned long long)pl.h * pl.ntiles * 64, 64, 64, 64, true);
+}
 inline bool is_dense(const TRef& r, long long L) { return r.dr == D && r.ts == D && r.hs == L * D; }
 inline int map_act(CUtensorMap* m, const TRef& r, long long L, int heads, bool dense) {  // bf16 64x64 SW128
   if (dense) return make_map(m, r.p, true, (unsigned long long)heads * L, D, 64, T, true);

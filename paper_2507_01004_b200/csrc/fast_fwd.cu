@@ -387,9 +387,13 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         ZTRACE(tr, 2, n);
         mbar_wait(s_ready, n & 1);
         if (save_sp) {  // chunk-start state for the backward: async bulk store straight from smem
-          const int rs = (hh * ntiles + t0 + n) * D;
-          tma_store_2d(&tm_sp, sp_buf, 0, rs);
-          tma_store_2d(&tm_sp, sp_buf + SPANEL, 64, rs);
+          if (dr == D) {
+            const int rs = (hh * ntiles + t0 + n) * D;
+            tma_store_2d(&tm_sp, sp_buf, 0, rs);
+            tma_store_2d(&tm_sp, sp_buf + SPANEL, 64, rs);
+          } else {  // d = 64: only the 64 x 64 block of real channels is nonzero
+            tma_store_2d(&tm_sp, sp_buf, 0, (hh * ntiles + t0 + n) * 64);
+          }
           tma_store_commit();
         }
         const uint32_t ob = n & 1;
@@ -686,7 +690,7 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   // pointer-addressed tensors (g, o) are dense
   const bool din = is_dense(q, pl.L) && is_dense(k, pl.L) && is_dense(v, pl.L);
   const bool dn = is_dense(g, pl.L) && is_dense(o, pl.L);
-  if (int rc = make_map(&msp, w.Sp, true, (unsigned long long)pl.h * pl.ntiles * D, D, 64, D, true)) return rc;
+  if (int rc = sp_map(&msp, w.Sp, pl, q.dr)) return rc;
   if (int rc = map_act(&mq, q, pl.L, pl.h, din)) return rc;
   if (int rc = map_act(&mk, k, pl.L, pl.h, din)) return rc;
   if (int rc = map_act(&mv, v, pl.L, pl.h, din)) return rc;
