@@ -110,3 +110,21 @@ def test_host_call_overlap_chain_matches():
     for a_set, b_set in zip(outs, want):
         for a, b in zip(a_set, b_set):
             assert torch.equal(a, b)
+
+
+def test_host_call_d64_vs_oracle():
+    """The host-buffer call on d = 64 heads (fused path with zero-filled channels)."""
+    from paper_2507_01004_b200 import distributed as zd
+    h, L, D = 4, 512, 64
+    host = _case(h, L, D, torch.bfloat16, seed=9)
+    layer = zd.ZecoRank(h, L, D, 64, torch.bfloat16)
+    assert layer.shard.fast
+    out = _outs(h, L, D, torch.bfloat16)
+    layer.forward_backward_host(host, out, head_groups=2)
+    torch.cuda.current_stream().synchronize()
+    q, k, v, g, do = (x.double().numpy() for x in host)
+    want_o, saved, _ = orc.zeco_forward(q, k, v, g, 1, 64)
+    want_g, _ = orc.zeco_backward(q, k, v, g, do, 1, 64, saved)
+    for name, a, b in zip(("o", "dq", "dk", "dv", "dg"), out, [want_o] + list(want_g)):
+        err = rel(a.double().numpy(), b)
+        assert err <= TOL_BF16, f"{name}: rel err {err:.3e}"

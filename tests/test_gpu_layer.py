@@ -26,10 +26,11 @@ def _inputs(h, L, d, dtype, seed=0, lo=math.log(0.9), hi=math.log(0.999)):
     return q, k, v, g, w
 
 
-@pytest.mark.parametrize("dtype,tol", [(torch.bfloat16, TOL_BF16), (torch.float32, TOL_F32)])
-def test_autograd_function_vs_torch_reference(dtype, tol):
+@pytest.mark.parametrize("dtype,tol,D", [(torch.bfloat16, TOL_BF16, 128), (torch.float32, TOL_F32, 128),
+                                         (torch.bfloat16, TOL_BF16, 64)])
+def test_autograd_function_vs_torch_reference(dtype, tol, D):
     from paper_2507_01004_b200.layer import gla_reference, zeco_gla
-    q, k, v, g, w = _inputs(2, 256, 128, dtype)
+    q, k, v, g, w = _inputs(2, 256, D, dtype)
     leaves = [x.clone().requires_grad_(True) for x in (q, k, v, g)]
     o = zeco_gla(*leaves)
     (o.double() * w).sum().backward()
@@ -78,3 +79,30 @@ def test_model_step_and_recompute_equivalence():
     assert res[0][0] == res[1][0]
     for a, b in zip(res[0][1], res[1][1]):
         assert torch.equal(a, b)
+
+
+def test_layer_d64_heads_strided_plumbing():
+    """32 x 64-style heads (4 x 64 here) through the layer: the zero-copy strided path (projection head
+    slices in, token-major outputs / gradients) must give exactly what dense copies give, and the output
+    must match the float64 reference core.  (x.grad is not compared against the reference: the per-head
+    RMS norm of rows with |o| ~1e-3 of the median amplifies bf16 rounding of the core output -- the
+    core's own gradients are checked against the reference in test_autograd_function_vs_torch_reference.)"""
+    from paper_2507_01004_b200.layer import GatedLinearAttention, gla_reference, zeco_gla
+    torch.manual_seed(1)
+    layer = GatedLinearAttention(hidden_size=256, num_heads=4, device="cuda")
+    x = (torch.randn(512, 256, device="cuda") * 0.5).to(torch.bfloat16)
+
+    def dense(q, k, v, g, *a):
+        return zeco_gla(q.contiguous(), k.contiguous(), v.contiguous(), g.contiguous()).contiguous()
+    outs = []
+    for core in (None, dense, gla_reference):
+        layer.zero_grad()
+        xx = x.clone().requires_grad_(True)
+        y = layer(xx, core)
+        y.float().square().mean().backward()
+        outs.append((y.detach(), xx.grad.clone(), [p.grad.clone() for p in layer.parameters()]))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert rel(outs[0][1], outs[1][1]) <= 1e-6
+    for a, b in zip(outs[0][2], outs[1][2]):
+        assert rel(a, b) <= 1e-6
+    assert rel(outs[0][0], outs[2][0]) <= TOL_BF16
