@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   if constexpr (DENSE) {  // compile-time strides for the dense layout
     gts = D, ghs = L * D;
     gs = Strides4{D, D, D, D, L * D, L * D, L * D, L * D};
+    dr = D;
   }
 
   if (tid == 0) {
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_do);
       tma_prefetch_desc(&tm_sp);
-      const uint64_t pol = ZGLA_CONSUMER_EVICT_FIRST ? l2_policy_evict_first() : l2_policy_evict_normal();
+      const uint64_t pol = ZGLA_CONSUMER_EVICT_FIRST ? l2_policy_evict_first() : 0;  // 0: no cache hint
       for (int m = 0; m < nt; ++m) {
         const int st = m % BO_NS, ph = (m / BO_NS) & 1;
         const int n = t1 - 1 - m;

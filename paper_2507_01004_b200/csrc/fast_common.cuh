@@ -21,7 +21,7 @@
 #define ZGLA_L2_KEEP_PCT 20  // percent of a producer walk (K1 / K4) loaded with normal L2 priority (tuned: 0.3995 -> 0.3895 ms)
 #endif
 #ifndef ZGLA_CONSUMER_EVICT_FIRST
-#define ZGLA_CONSUMER_EVICT_FIRST 0  // consumer kernels (K3 / K6) load with evict-first priority
+#define ZGLA_CONSUMER_EVICT_FIRST 0  // consumer kernels (K3 / K6): 1 = evict-first hint, 0 = plain loads
 #endif
 
 namespace zgla {
@@ -208,10 +208,17 @@ inline int map_gate(CUtensorMap* m, const TRef& r, long long L, int heads, bool 
 template <bool DENSE>
 __device__ __forceinline__ void tile_load(void* dst, const CUtensorMap* m, uint64_t* bar, int col, int t, int hh,
                                           long long L, int in3d, uint64_t policy) {
-  if (!in3d)
-    tma_load_2d_hint(dst, m, bar, col, (int)(hh * L + t), policy);
-  else
-    tma_load_3d_hint(dst, m, bar, col, t, hh, policy);
+  if (!in3d) {
+    if (policy)
+      tma_load_2d_hint(dst, m, bar, col, (int)(hh * L + t), policy);
+    else
+      tma_load_2d(dst, m, bar, col, (int)(hh * L + t));
+  } else {
+    if (policy)
+      tma_load_3d_hint(dst, m, bar, col, t, hh, policy);
+    else
+      tma_load_3d(dst, m, bar, col, t, hh);
+  }
 }
 
 // ---- optional pipeline tracing (diagnostics): CTA g_trace_cta records %globaltimer per (event, tile)

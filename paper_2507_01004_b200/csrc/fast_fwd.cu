@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   if constexpr (DENSE) {  // compile-time strides for the dense layout
     gts = D, ots = D;
     ghs = L * D, ohs = L * D;
+    dr = D;
   }
 
   if (tid == 0) {
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_g);
-      const uint64_t pol = ZGLA_CONSUMER_EVICT_FIRST ? l2_policy_evict_first() : l2_policy_evict_normal();
+      const uint64_t pol = ZGLA_CONSUMER_EVICT_FIRST ? l2_policy_evict_first() : 0;  // 0: no cache hint
       for (int n = 0; n < nt; ++n) {
         const int st = n % FO_NS, ph = (n / FO_NS) & 1;
         uint8_t* sb = smem + st * FO_STAGE;
