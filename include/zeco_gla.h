@@ -113,6 +113,11 @@ int zgla_zeco_bwd_output(const zgla_shape* s, int num_sms, const void* q, const 
                          const void* g, const void* d_out, void* ws, const void* s_prev, const void* ds_next,
                          void* dq, void* dk, void* dv, void* dg, void* stream);
 
+/* after zgla_zeco_fwd_local: ZGLA_ERR_DOMAIN if a 64-token tile's summed log-decay was below -160 (or
+ * not finite) on the fused bf16 path, whose in-tile exponents e^{+-(logb - r)} would overflow there;
+ * synchronises `stream` (a validation call, not for the timed path).  ZGLA_OK on the SIMT paths. */
+int zgla_zeco_domain_check(const zgla_shape* s, int num_sms, const void* ws, void* stream);
+
 /* the same four entry points over strided tensors (zgla_tensor); ZGLA_ERR_LAYOUT if a stride or base is
  * not 16-byte aligned, or if the shape runs the SIMT path and a tensor is not dense */
 int zgla_zeco_fwd_local_v(const zgla_shape* s, int num_sms, const zgla_tensor* k, const zgla_tensor* v,

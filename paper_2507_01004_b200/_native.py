@@ -69,6 +69,7 @@ _SIGS = {
     "zgla_zeco_fwd_output": ([ctypes.POINTER(Shape), _I, _P, _P, _P, _P, _P, _P, _P, _P], _I),
     "zgla_zeco_bwd_local": ([ctypes.POINTER(Shape), _I, _P, _P, _P, _P, _P, _P], _I),
     "zgla_zeco_bwd_output": ([ctypes.POINTER(Shape), _I] + [_P] * 13, _I),
+    "zgla_zeco_domain_check": ([ctypes.POINTER(Shape), _I, _P, _P], _I),
     "zgla_zeco_fwd_local_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _P, _P, _P, _P], _I),
     "zgla_zeco_fwd_output_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _T, _P, _P, _T, _P], _I),
     "zgla_zeco_bwd_local_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _P, _P, _P], _I),

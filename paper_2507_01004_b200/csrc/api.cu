@@ -38,6 +38,7 @@ namespace fast {
 struct TRef;
 }
 bool fast_supported(const zgla_shape* s);
+int fast_domain_flag(const zgla_shape* s, int num_sms, const void* ws, int* host_flag, cudaStream_t st);
 long long fast_ws_bytes(const zgla_shape* s, int num_sms);
 int fast_fwd_local(const zgla_shape*, int, const fast::TRef&, const fast::TRef&, const fast::TRef&, void*, void*,
                    void*, cudaStream_t);
@@ -190,4 +191,17 @@ extern "C" int zgla_zeco_bwd_output(const zgla_shape* s, int num_sms, const void
   const zgla_tensor tq = dn(q), tk = dn(k), tv = dn(v), tg = dn(g), td = dn(d_out);
   const zgla_tensor a = dn(dq), b = dn(dk), c = dn(dv), e = dn(dg);
   return zgla_zeco_bwd_output_v(s, num_sms, &tq, &tk, &tv, &tg, &td, ws, s_prev, ds_next, &a, &b, &c, &e, stream);
+}
+
+extern "C" int zgla_zeco_domain_check(const zgla_shape* s, int num_sms, const void* ws, void* stream) {
+  if (int rc = validate_zeco(s, num_sms)) return rc;
+  if (!fast_supported(s)) return ZGLA_OK;  // the SIMT paths use the exact token recurrence: any gate
+  int flag = 0;
+  if (int rc = fast_domain_flag(s, num_sms, ws, &flag, (cudaStream_t)stream)) return rc;
+  if (flag) {
+    set_error("a 64-token tile's log-decay is below -160 (or not finite): outside the fused bf16 path's "
+              "exponent domain; use the fp32 validation mode for such gates");
+    return ZGLA_ERR_DOMAIN;
+  }
+  return ZGLA_OK;
 }

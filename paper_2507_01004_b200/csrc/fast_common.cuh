@@ -57,13 +57,18 @@ struct Ws {
   float* Dend;    // [h][nseg][D][D]  bwd: rank-local cotangent at segment end (later segments)
   float* cumGr;   // [h][nseg][D]     sum of gam over later segments
   __nv_bfloat16* Sp;  // [h][NT][D][D] bf16: scaled chunk-start states e^{r} S for the backward
+  int* flags;         // [0]: a 64-token tile's log-decay left the fast path's exponent domain
 };
+
+// The fused kernels scale q / k by e^{+-(logb - r)} with r the tile's middle row, so a tile whose total
+// log-decay is below -2 * DOMAIN_EXP overflows fp32 / bf16.  The forward segment pass flags it.
+constexpr float DOMAIN_EXP = 80.f;
 
 inline long long ws_bytes(const Plan& p) {
   const long long st = (long long)p.h * p.nseg * D * D * 4;
   const long long vec = (long long)p.h * p.nseg * D * 4;
   const long long sp = (long long)p.h * p.ntiles * STATE_BF16;
-  return 4 * st + 3 * vec + sp + 4096;
+  return 4 * st + 3 * vec + sp + 4096 + 256;
 }
 
 inline Ws carve(const Plan& p, void* base) {
@@ -81,6 +86,7 @@ inline Ws carve(const Plan& p, void* base) {
   uintptr_t sp = reinterpret_cast<uintptr_t>(w.cumGr + vec);
   sp = (sp + 1023) & ~uintptr_t(1023);
   w.Sp = reinterpret_cast<__nv_bfloat16*>(sp);
+  w.flags = reinterpret_cast<int*>(sp + (uintptr_t)p.h * p.ntiles * STATE_BF16);
   return w;
 }
 

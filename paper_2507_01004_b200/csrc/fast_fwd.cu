@@ -32,7 +32,7 @@ template <int DIR, bool DENSE>  // 0: forward local state (a=k, b=v, reverse wal
 __global__ void __launch_bounds__(KS_THREADS, 1)
     seg_state_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                      const __grid_constant__ CUtensorMap tm_g, long long L, int in3d, int nseg, int ntiles,
-                     float* __restrict__ out_state, float* __restrict__ out_gam) {
+                     float* __restrict__ out_state, float* __restrict__ out_gam, int* __restrict__ flags) {
   extern __shared__ uint8_t smem_raw[];
   // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
 #pragma unroll
       for (int r = 1; r < 64; ++r) lb[r] += lb[r - 1];
       const float gam = lb[63];
+      if (DIR == 0 && flags != nullptr && !(gam >= -2.f * DOMAIN_EXP)) atomicOr(flags, 1);  // also catches NaN
       xg[(i & 3) * D + c] = gam;
       mbar_arrive(&gready[i & 3]);
       if (i >= 1) {  // gamma of tile i-1 (other group)
@@ -656,7 +657,7 @@ bool fast_supported(const zgla_shape* s) {
 long long fast_ws_bytes(const zgla_shape* s, int num_sms) { return ws_bytes(make_plan(s, num_sms)); }
 
 int launch_seg_state(int dir, const Plan& pl, const TRef& a, const TRef& b, const TRef& g, float* out_state,
-                     float* out_gam, cudaStream_t st) {
+                     float* out_gam, int* flags, cudaStream_t st) {
   CUtensorMap ma, mb, mg;
   const bool dn = is_dense(a, pl.L) && is_dense(b, pl.L) && is_dense(g, pl.L);  // all TMA-read
   if (int rc = map_act(&ma, a, pl.L, pl.h, dn)) return rc;
@@ -665,7 +666,7 @@ int launch_seg_state(int dir, const Plan& pl, const TRef& a, const TRef& b, cons
   auto kern = dir == 0 ? seg_state_kernel<0, true> : seg_state_kernel<1, true>;
   set_smem_once((const void*)kern, (int)KS_SMEM);
   if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, KS_THREADS, KS_SMEM, st, ma, mb, mg, pl.L, dn ? 0 : 1, pl.nseg,
-                                pl.ntiles, out_state, out_gam))
+                                pl.ntiles, out_state, out_gam, flags))
     return cuda_fail(e, "seg_state_kernel");
   return zgla_check_launch();
 }
@@ -674,7 +675,8 @@ int fast_fwd_local(const zgla_shape* s, int num_sms, const TRef& k, const TRef& 
                    void* s_local, void* g_tot, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
-  if (int rc = launch_seg_state(0, pl, k, v, g, w.dS, w.gam, st)) return rc;
+  if (cudaError_t e = cudaMemsetAsync(w.flags, 0, sizeof(int), st)) return cuda_fail(e, "fast_fwd_local");
+  if (int rc = launch_seg_state(0, pl, k, v, g, w.dS, w.gam, w.flags, st)) return rc;
   const long long n = (long long)pl.h * D * D;
   if (cudaError_t e = launch_k(fwd_scan_kernel, (unsigned)((n + 255) / 256), 256, 0, st, pl.h, pl.nseg, k.dr,
                                 (const float*)w.dS, (const float*)w.gam, w.Sin, w.cumG, (float*)s_local, (float*)g_tot))
@@ -711,7 +713,7 @@ int fast_bwd_local(const zgla_shape* s, int num_sms, const TRef& q, const TRef& 
                    void* ds0, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
-  if (int rc = launch_seg_state(1, pl, q, d_out, g, w.dD, w.gam, st)) return rc;
+  if (int rc = launch_seg_state(1, pl, q, d_out, g, w.dD, w.gam, nullptr, st)) return rc;
   const long long n = (long long)pl.h * D * D;
   if (cudaError_t e = launch_k(bwd_scan_kernel, (unsigned)((n + 255) / 256), 256, 0, st, pl.h, pl.nseg, q.dr,
                                 (const float*)w.dD, (const float*)w.gam, w.Dend, w.cumGr, (float*)ds0))
@@ -719,4 +721,15 @@ int fast_bwd_local(const zgla_shape* s, int num_sms, const TRef& q, const TRef& 
   return zgla_check_launch();
 }
 
+}  // namespace zgla
+
+namespace zgla {
+int fast_domain_flag(const zgla_shape* s, int num_sms, const void* ws, int* host_flag, cudaStream_t st) {
+  const Plan pl = make_plan(s, num_sms);
+  Ws w = carve(pl, const_cast<void*>(ws));
+  if (cudaError_t e = cudaMemcpyAsync(host_flag, w.flags, sizeof(int), cudaMemcpyDeviceToHost, st))
+    return cuda_fail(e, "zgla_zeco_domain_check");
+  if (cudaError_t e = cudaStreamSynchronize(st)) return cuda_fail(e, "zgla_zeco_domain_check");
+  return ZGLA_OK;
+}
 }  // namespace zgla

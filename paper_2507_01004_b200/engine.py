@@ -187,6 +187,9 @@ def run_forward(seq: GlobalSequence, strategy: StrategyKind, cluster: DeviceClus
             with cluster.phase(r, "local_scan"):
                 q, k, v, g = ranks[r]
                 loc.append(shards[r].fwd_local(k, v, g))
+        for sh in shards:  # the fused bf16 path's exponent domain (DomainError, like invalid gates)
+            if sh.fast:
+                sh.check_domain()
         finals = torch.stack([x[0] for x in loc])
         totals = torch.stack([x[1] for x in loc])
         if strategy is StrategyKind.LASP2 and P > 1:

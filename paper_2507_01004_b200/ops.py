@@ -288,6 +288,11 @@ class ZecoShard:
                      self._ref(g), _p(self.ws), _p(s_local), _p(g_tot), _stream())
         return s_local, g_tot
 
+    def check_domain(self):
+        """DomainError if the last fwd_local saw a tile whose log-decay overflows the fused path's exponents
+        (synchronises; a validation step, not for the timed path)."""
+        _native.call("zgla_zeco_domain_check", ctypes.byref(self.shape), self.sms, _p(self.ws), _stream())
+
     def fwd_output(self, q, k, v, g, s_prev=None, out=None):
         """outputs [h, L, dv]; ``out`` may be a strided view (e.g. of a token-major [L, h * dv] buffer)."""
         geo = self.geo

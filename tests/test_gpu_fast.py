@@ -221,3 +221,23 @@ def test_fast_d64_heads_against_oracle(P, L, h, long_memory):
     want = oracle(q, k, v, g, do, P)
     check(got, want)
     assert rel(got["prev"], want["prev"]) <= TOL_BF16
+
+
+def test_fast_domain_flag():
+    """A tile whose summed log-decay is below -160 (per-token decay < ~0.08) is outside the fused path's
+    exponent domain: check_domain() raises DomainError; gates inside the domain pass."""
+    from paper_2507_01004_b200 import ops
+    from paper_2507_01004_b200.errors import DomainError
+    h, L, D = 2, 512, 128
+    sh = ops.ZecoShard(h, L, D, D, 64, torch.bfloat16)
+    k, v = ((torch.rand(h, L, D, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(2))
+    g = torch.full((h, L, D), math.log(0.5), device="cuda")  # tile total 64 * -0.69 = -44: fine
+    sh.fwd_local(k, v, g)
+    sh.check_domain()
+    g[1, 200, 7] = -200.0  # one strong gate makes its tile leave the domain
+    sh.fwd_local(k, v, g)
+    with pytest.raises(DomainError):
+        sh.check_domain()
+    g[1, 200, 7] = math.log(0.5)
+    sh.fwd_local(k, v, g)  # the flag is per call
+    sh.check_domain()
