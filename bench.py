@@ -394,7 +394,7 @@ def main():
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                 "call": f"ZecoRank.forward_backward_host -> zgla_zeco_fwd_bwd_host, pinned host buffers, "
                         f"{args.e2e_groups} head groups pipelined H2D/kernels/D2H, consecutive steps chained"},
-        "gpu_launches": args.steps * (6 + (4 if world > 1 else 0)),
+        "gpu_launches": args.steps * (6 + (2 if world > 1 else 0)),  # + the two All-Scan chain kernels
         "clocks": clk.summary(),
     }
     if world > 1:
