@@ -264,7 +264,7 @@ def main():
     def step(evs=None):
         def mark(i):
             if evs is not None:
-                evs[i].record(stream)
+                evs[i].record()  # current stream: the capture stream while a graph is being captured
         mark(0)
         s_loc, g_tot = layer.shard.fwd_local(k, v, g)
         mark(1)
@@ -307,6 +307,12 @@ def main():
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             step()
+        # a second capture of the same step with timing-event nodes between the phases: per-kernel times
+        # of graph-launched kernels (event nodes cost ~4 us each, so this graph is not the timed one)
+        graph_ev = torch.cuda.CUDAGraph()
+        graph_evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(7)]
+        with torch.cuda.graph(graph_ev):
+            step(graph_evs)
         for _ in range(3):
             graph.replay()
     run_step = graph.replay if graph is not None else step
@@ -324,6 +330,15 @@ def main():
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end)
+    # per-phase kernel times from replays of the evented graph (mean of 10), else the eager pass
+    phase_timed = per_phase
+    if graph is not None:
+        samples = []
+        for _ in range(10):
+            graph_ev.replay()
+            torch.cuda.synchronize()
+            samples.append([graph_evs[j].elapsed_time(graph_evs[j + 1]) for j in range(len(phases))])
+        phase_timed = {p: statistics.mean(x[j] for x in samples) for j, p in enumerate(phases)}
     if world > 1:
         ms = max_over_ranks(ms)
     ms_step = ms / args.steps
@@ -361,10 +376,10 @@ def main():
     fwd_b, bwd_b = bytes_per_token_head(D, D)
     fwd_f, bwd_f = flops_per_token_head(C, D, D)
     units = H * L
-    dom = max(("fwd_output", "bwd_output", "fwd_local", "bwd_local"), key=lambda p: per_phase[p])
+    dom = max(("fwd_output", "bwd_output", "fwd_local", "bwd_local"), key=lambda p: phase_timed[p])
     dom_bytes = {"fwd_output": fwd_b, "bwd_output": bwd_b, "fwd_local": 2 * D + 2 * D + 4 * D,
                  "bwd_local": 2 * D + 2 * D + 4 * D}[dom] * units
-    dom_ms = per_phase[dom]
+    dom_ms = phase_timed[dom]
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     step_bytes = (fwd_b + bwd_b) * units
     step_flops = (fwd_f + bwd_f) * units
@@ -378,7 +393,8 @@ def main():
                    "allscan_blocks": args.blocks, "parallelism": f"zeco-sp{world}",
                    "l2": "inputs 384 MiB per GPU > 126 MiB L2 (no flush needed)"},
         "per_gpu_tokens_per_s": L / (ms_step / 1e3),
-        "phase_ms": {p: round(per_phase[p], 5) for p in phases},
+        "phase_ms": {p: round(phase_timed[p], 5) for p in phases},  # graph-launched (event nodes between)
+        "phase_ms_eager": {p: round(per_phase[p], 5) for p in phases},
         "timed_as": "cuda_graph" if graph is not None else "eager",
         "roofline": {"kernel": {"fwd_output": "fwd_out_kernel", "bwd_output": "bwd_out_kernel",
                                 "fwd_local": "seg_state_kernel<0>+fwd_scan", "bwd_local": "seg_state_kernel<1>+bwd_scan"}[dom],
