@@ -132,8 +132,9 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  pdl_wait();
+  // only the epilogue warps' prologue reads the preceding scan's outputs (Dend, cumGr)
   pdl_trigger();
+  if (warp < 8) pdl_wait();
 
   if (warp == 12) {
     // ---------------- TMA producer (tiles right to left)
@@ -512,7 +513,7 @@ int fast_bwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   const Strides4 gs{(int)dq.ts, (int)dk.ts, (int)dv.ts, (int)dg.ts, dq.hs, dk.hs, dv.hs, dg.hs};
   auto kern = dn ? bwd_out_kernel<true> : bwd_out_kernel<false>;
   set_smem_once((const void*)kern, (int)BO_SMEM);
-  if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp, mg,
+  if (cudaError_t e = launch_kp(ZGLA_EARLY || pdl_enabled(), kern, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp, mg,
                                 (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
                                 (const float*)w.Sin, (const float*)w.cumG, (const float*)w.dS, (const float*)w.gam, (const float*)s_prev,
                                 (const float*)w.Dend, (const float*)w.cumGr, (const float*)ds_next,

@@ -281,6 +281,24 @@ inline bool pdl_enabled() {
 }
 
 template <typename... Exp, typename... Act>
+inline cudaError_t launch_kp(bool pdl, void (*kern)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                             Act&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
+}
+#ifndef ZGLA_EARLY
+#define ZGLA_EARLY 0
+#endif
+template <typename... Exp, typename... Act>
 inline cudaError_t launch_k(void (*kern)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                             Act&&... args) {
   cudaLaunchConfig_t cfg = {};

@@ -337,8 +337,10 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  pdl_wait();
+  // Only the state warps read the preceding scan's outputs (Sin, cumG): with an early launch the
+  // loads of q / k / v / g and the per-tile prep run while that kernel is still finishing.
   pdl_trigger();
+  if (warp < 4) pdl_wait();
 
   if (warp == 12) {
     // ---------------- TMA producer
@@ -700,7 +702,7 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   if (int rc = map_gate(&mg, g, pl.L, pl.h, din && is_dense(g, pl.L))) return rc;
   auto kern = dn ? fwd_out_kernel<true> : fwd_out_kernel<false>;
   set_smem_once((const void*)kern, (int)FO_SMEM);
-  if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
+  if (cudaError_t e = launch_kp(ZGLA_EARLY || pdl_enabled(), kern, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
                                 (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
                                 (const float*)w.Sin, (const float*)w.cumG, (const float*)s_prev, (__nv_bfloat16*)o.p,
                                 o.ts, o.hs, w.Sp,
