@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   if (tid == 0) {
     for (int i = 0; i < BO_NS; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 256);
+      mbar_init(&empty[i], 256 + 1);  // the epilogue's reads of Qh / Kh + the MMA warp's last commit
       mbar_init(&prep[i], 128);
     }
     mbar_init(sc_full, 1);
@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           mma_bf16_ss(tbase + BC_QDO, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(da + kk * 2048, PANEL, 1024),
                       id_qdo, 1);
         mma_commit(qdo_full);
+        mma_commit(&empty[st]);  // QDO reads q / dO of this stage
         ZTRACE(tr, 4, m);
       }
     }
@@ -333,16 +334,21 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           const bool inb = c < dr && 64 * ch + jj < dr;
           if (ds_next && inb) {
             const float4 a = *reinterpret_cast<const float4*>(ds_next + pidx + jj);
-            dd.x += cgr * a.x; dd.y += cgr * a.y; dd.z += cgr * a.z; dd.w += cgr * a.w;
+            dd.x = fmaf(cgr, a.x, dd.x); dd.y = fmaf(cgr, a.y, dd.y);
+            dd.z = fmaf(cgr, a.z, dd.z); dd.w = fmaf(cgr, a.w, dd.w);
           }
           if (s_prev && inb) {
             const float4 a = *reinterpret_cast<const float4*>(s_prev + pidx + jj);
-            si.x += cg * a.x; si.y += cg * a.y; si.z += cg * a.z; si.w += cg * a.w;
+            si.x = fmaf(cg, a.x, si.x); si.y = fmaf(cg, a.y, si.y);
+            si.z = fmaf(cg, a.z, si.z); si.w = fmaf(cg, a.w, si.w);
           }
           dv32[j] = dd.x; dv32[j + 1] = dd.y; dv32[j + 2] = dd.z; dv32[j + 3] = dd.w;
           // fp32 forward state at the segment end: e^{gam_s} S_in + dS_s
-          rho += (eg * si.x + ds.x) * dd.x + (eg * si.y + ds.y) * dd.y + (eg * si.z + ds.z) * dd.z +
-                 (eg * si.w + ds.w) * dd.w;
+          // explicit FMAs: the same rounding in every kernel variant
+          rho = fmaf(fmaf(eg, si.x, ds.x), dd.x, rho);
+          rho = fmaf(fmaf(eg, si.y, ds.y), dd.y, rho);
+          rho = fmaf(fmaf(eg, si.z, ds.z), dd.z, rho);
+          rho = fmaf(fmaf(eg, si.w, ds.w), dd.w, rho);
         }
         tmem_st32(d_addr + 32 * hf, dv32);  // Dt at the segment end (frame r = 0)
       }
@@ -454,7 +460,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           const int i = 8 * h8 + u;
           const float q_raw = __uint_as_float(gq[u]), k_raw = __uint_as_float(gk[u]);
           const float dlt = __uint_as_float(dl[u]) * LOG2E;
-          da[i] = qh[u] * q_raw - kh[u] * k_raw;
+          da[i] = __fsub_rn(__fmul_rn(qh[u], q_raw), __fmul_rn(kh[u], k_raw));  // no FMA contraction: identical in every variant
           tsum += da[i];
           if (DENSE || c < dr) {  // channels of a d = 64 head beyond 64 are padding
             *pdq = __float2bfloat16_rn(q_raw * fast_exp2(dlt));
