@@ -1,5 +1,8 @@
+"""Layer-level d=64 debugging: GLA core gradients vs the float64 torch reference, per tensor and through
+the layer (the per-head RMS norm of near-zero rows amplifies bf16 rounding; see tests/test_gpu_layer.py)."""
 import sys, torch
-sys.path.insert(0, '/root/repo')
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2507_01004_b200.layer import GatedLinearAttention, gla_reference, zeco_gla
 def rel(a, b):
     a, b = a.double(), b.double(); s = max(a.norm().item(), b.norm().item()); return (a - b).norm().item() / s
