@@ -70,3 +70,28 @@ def test_invalid_shapes_rejected_before_any_launch():
     ok = _native.Shape(heads=16, key_dim=128, value_dim=128, chunk_len=64, seq_len=16384, dtype=_native.ZGLA_BF16)
     assert lib.zgla_zeco_workspace_bytes(ctypes.byref(ok), 148) > 0
     assert lib.zgla_allscan_local(2, 1, 4, 4, _native.ZGLA_F32, 3, 0, None, None, None, None, None) == -4
+
+
+def test_plain_c_client_compiles_and_links(tmp_path):
+    """The header is plain C99 and the library links into a C program (no torch / C++ in the ABI)."""
+    import os
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "client.c"
+    src.write_text(
+        '#include "zeco_gla.h"\n#include <stdio.h>\n'
+        "int main(void) {\n"
+        "  zgla_shape s = {16, 128, 128, 64, 16384, ZGLA_BF16};\n"
+        "  zgla_tensor t = {0, 0, 0};\n  (void)t;\n"
+        "  long long ws = zgla_zeco_workspace_bytes(&s, 148);\n"
+        '  printf("%s %lld\\n", zgla_version(), ws);\n'
+        "  return ws > 0 ? 0 : 1;\n}\n")
+    lib = os.path.join(root, "paper_2507_01004_b200")
+    exe = tmp_path / "client"
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(root, "include"), str(src),
+                    "-L", lib, "-lzeco_gla", f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert out.startswith("zeco-gla-b200")
