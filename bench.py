@@ -397,7 +397,7 @@ def main():
         "phase_ms_eager": {p: round(per_phase[p], 5) for p in phases},
         "timed_as": "cuda_graph" if graph is not None else "eager",
         "roofline": {"kernel": {"fwd_output": "fwd_out_kernel", "bwd_output": "bwd_out_kernel",
-                                "fwd_local": "seg_state_kernel<0>+fwd_scan", "bwd_local": "seg_state_kernel<1>+bwd_scan"}[dom],
+                                "fwd_local": "seg_state_kernel<0>+seg_scan_kernel<0>", "bwd_local": "seg_state_kernel<1>+seg_scan_kernel<1>"}[dom],
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": load_traffic(), "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": dom_bytes},

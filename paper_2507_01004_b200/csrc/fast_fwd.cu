@@ -5,7 +5,7 @@
 //   seg_state_kernel<BWD>  (K4)  dD_s  = sum_t e^{G_t - G_start} q_t^T dO_t   forward tile walk
 //       one TMEM accumulator per CTA; every coefficient is <= 1, so the whole
 //       segment is ONE uninterrupted tcgen05 accumulation (no TMEM round trips)
-//   fwd_scan_kernel / bwd_scan_kernel (K2/K5): elementwise scans over segments
+//   seg_scan_kernel<0> / <1> (K2/K5): elementwise scans over segments
 //   fwd_out_kernel (K3): per 64-token tile
 //       A   = Qh Kh^T               (M=64,  N=64,  K=128)  scores, masked in registers
 //       O   = Qh (e^{r} S)         (M=64,  N=128, K=128)  inter-chunk term
@@ -183,76 +183,61 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
 
 // ============================================================== K2 / K5
 // forward: Sin[s] = sum_{s'<s} e^{gam(s'+1..s-1)} dS[s'];  S_local = inclusive;  cumG / G_tot
-// One thread per state element walks the segments in order; the loads of a batch of SCAN_B segments
+// backward: Dend[s] = sum_{s'>s} e^{gam(s+1..s'-1)} dD[s'];  ds_local0 = inclusive of all;  cumGr
+// One thread per four state elements walks the segments in order; the loads of a batch of SCAN_B segments
 // are issued before the dependent multiply-adds, so the walk costs ~nseg/SCAN_B memory latencies
 // instead of nseg.
-constexpr int SCAN_B = 8;
+#ifndef ZGLA_SCAN_B
+#define ZGLA_SCAN_B 8
+#endif
+constexpr int SCAN_B = ZGLA_SCAN_B;
 
-__global__ void fwd_scan_kernel(int h, int nseg, int dr, const float* __restrict__ dS,
-                                const float* __restrict__ gam, float* __restrict__ Sin, float* __restrict__ cumG,
-                                float* __restrict__ s_local, float* __restrict__ g_tot) {
-  pdl_wait();
-  pdl_trigger();
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)h * D * D) return;
-  const int hh = (int)(idx / (D * D)), e = (int)(idx % (D * D)), c = e % D, vv = e / D;
-  const long long base = (long long)hh * nseg * D * D + e;
-  const float* gm = gam + (long long)hh * nseg * D + c;
-  float run = 0.f, cm = 0.f;
-  for (int s0 = 0; s0 < nseg; s0 += SCAN_B) {
-    float x[SCAN_B], gg[SCAN_B];
-#pragma unroll
-    for (int j = 0; j < SCAN_B; ++j) {
-      const bool ok = s0 + j < nseg;
-      x[j] = ok ? __ldcs(dS + base + (long long)(s0 + j) * D * D) : 0.f;
-      gg[j] = ok ? __ldg(gm + (s0 + j) * D) : 0.f;
-    }
-#pragma unroll
-    for (int j = 0; j < SCAN_B; ++j) {
-      if (s0 + j < nseg) {
-        Sin[base + (long long)(s0 + j) * D * D] = run;
-        run = expf(gg[j]) * run + x[j];
-        if (vv == 0) cumG[(long long)(hh * nseg + s0 + j) * D + c] = cm;
-        cm += gg[j];
-      }
-    }
-  }
-  // API layout: row-major [h][dr][dr] (the padded channels of d = 64 heads are dropped)
-  if (s_local && c < dr && vv < dr) s_local[((long long)hh * dr + c) * dr + vv] = run;
-  if (vv == 0 && g_tot && c < dr) g_tot[hh * dr + c] = cm;
+__device__ __forceinline__ float4 f4_fma_exp(float4 g, float4 r, float4 x) {
+  return make_float4(expf(g.x) * r.x + x.x, expf(g.y) * r.y + x.y, expf(g.z) * r.z + x.z, expf(g.w) * r.w + x.w);
 }
-
-// backward: Dend[s] = sum_{s'>s} e^{gam(s+1..s'-1)} dD[s'];  ds_local0 = Dend[-1] inclusive of all; cumGr
-__global__ void bwd_scan_kernel(int h, int nseg, int dr, const float* __restrict__ dD,
-                                const float* __restrict__ gam, float* __restrict__ Dend, float* __restrict__ cumGr,
-                                float* __restrict__ ds0) {
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+// DIR 0 (K2): Sin / cumG / S_local / G_tot;  DIR 1 (K5): Dend / cumGr / ds_local0 (segments walked
+// from the last).  Four adjacent channels per thread: 16-byte loads and stores.
+template <int DIR>
+__global__ void seg_scan_kernel(int h, int nseg, int dr, const float* __restrict__ dS, const float* __restrict__ gam,
+                                float* __restrict__ Sin, float* __restrict__ cumG, float* __restrict__ s_local,
+                                float* __restrict__ g_tot) {
   pdl_wait();
   pdl_trigger();
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long idx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (idx >= (long long)h * D * D) return;
   const int hh = (int)(idx / (D * D)), e = (int)(idx % (D * D)), c = e % D, vv = e / D;
   const long long base = (long long)hh * nseg * D * D + e;
   const float* gm = gam + (long long)hh * nseg * D + c;
-  float run = 0.f, cm = 0.f;
-  for (int s0 = nseg - 1; s0 >= 0; s0 -= SCAN_B) {
-    float x[SCAN_B], gg[SCAN_B];
+  float4 run = make_float4(0.f, 0.f, 0.f, 0.f), cm = run;
+  for (int b0 = 0; b0 < nseg; b0 += SCAN_B) {
+    float4 x[SCAN_B], gg[SCAN_B];
 #pragma unroll
     for (int j = 0; j < SCAN_B; ++j) {
-      const bool ok = s0 - j >= 0;
-      x[j] = ok ? __ldcs(dD + base + (long long)(s0 - j) * D * D) : 0.f;
-      gg[j] = ok ? __ldg(gm + (s0 - j) * D) : 0.f;
+      const int s = DIR == 0 ? b0 + j : nseg - 1 - b0 - j;
+      const bool ok = b0 + j < nseg;
+      x[j] = ok ? __ldcs(reinterpret_cast<const float4*>(dS + base + (long long)s * D * D)) : make_float4(0, 0, 0, 0);
+      gg[j] = ok ? __ldg(reinterpret_cast<const float4*>(gm + s * D)) : make_float4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int j = 0; j < SCAN_B; ++j) {
-      if (s0 - j >= 0) {
-        Dend[base + (long long)(s0 - j) * D * D] = run;
-        run = expf(gg[j]) * run + x[j];
-        if (vv == 0) cumGr[(long long)(hh * nseg + s0 - j) * D + c] = cm;
-        cm += gg[j];
+      if (b0 + j < nseg) {
+        const int s = DIR == 0 ? b0 + j : nseg - 1 - b0 - j;
+        *reinterpret_cast<float4*>(Sin + base + (long long)s * D * D) = run;
+        run = f4_fma_exp(gg[j], run, x[j]);
+        if (vv == 0) *reinterpret_cast<float4*>(cumG + (long long)(hh * nseg + s) * D + c) = cm;
+        cm = f4_add(cm, gg[j]);
       }
     }
   }
-  if (ds0 && c < dr && vv < dr) ds0[((long long)hh * dr + c) * dr + vv] = run;
+  const float rv[4] = {run.x, run.y, run.z, run.w}, cv[4] = {cm.x, cm.y, cm.z, cm.w};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (s_local && c + u < dr && vv < dr) s_local[((long long)hh * dr + c + u) * dr + vv] = rv[u];
+    if (DIR == 0 && vv == 0 && g_tot && c + u < dr) g_tot[hh * dr + c + u] = cv[u];
+  }
 }
 
 // ============================================================== K3: forward outputs
@@ -680,9 +665,9 @@ int fast_fwd_local(const zgla_shape* s, int num_sms, const TRef& k, const TRef& 
   if (cudaError_t e = cudaMemsetAsync(w.flags, 0, sizeof(int), st)) return cuda_fail(e, "fast_fwd_local");
   if (int rc = launch_seg_state(0, pl, k, v, g, w.dS, w.gam, w.flags, st)) return rc;
   const long long n = (long long)pl.h * D * D;
-  if (cudaError_t e = launch_k(fwd_scan_kernel, (unsigned)((n + 255) / 256), 256, 0, st, pl.h, pl.nseg, k.dr,
+  if (cudaError_t e = launch_k(seg_scan_kernel<0>, (unsigned)((n / 4 + 127) / 128), 128, 0, st, pl.h, pl.nseg, k.dr,
                                 (const float*)w.dS, (const float*)w.gam, w.Sin, w.cumG, (float*)s_local, (float*)g_tot))
-    return cuda_fail(e, "fwd_scan_kernel");
+    return cuda_fail(e, "seg_scan_kernel<0>");
   return zgla_check_launch();
 }
 
@@ -717,9 +702,9 @@ int fast_bwd_local(const zgla_shape* s, int num_sms, const TRef& q, const TRef& 
   Ws w = carve(pl, ws);
   if (int rc = launch_seg_state(1, pl, q, d_out, g, w.dD, w.gam, nullptr, st)) return rc;
   const long long n = (long long)pl.h * D * D;
-  if (cudaError_t e = launch_k(bwd_scan_kernel, (unsigned)((n + 255) / 256), 256, 0, st, pl.h, pl.nseg, q.dr,
-                                (const float*)w.dD, (const float*)w.gam, w.Dend, w.cumGr, (float*)ds0))
-    return cuda_fail(e, "bwd_scan_kernel");
+  if (cudaError_t e = launch_k(seg_scan_kernel<1>, (unsigned)((n / 4 + 127) / 128), 128, 0, st, pl.h, pl.nseg, q.dr,
+                                (const float*)w.dD, (const float*)w.gam, w.Dend, w.cumGr, (float*)ds0, (float*)nullptr))
+    return cuda_fail(e, "seg_scan_kernel<1>");
   return zgla_check_launch();
 }
 
