@@ -57,7 +57,8 @@ struct Ws {
   float* Dend;    // [h][nseg][D][D]  bwd: rank-local cotangent at segment end (later segments)
   float* cumGr;   // [h][nseg][D]     sum of gam over later segments
   __nv_bfloat16* Sp;  // [h][NT][D][D] bf16: scaled chunk-start states e^{r} S for the backward
-  int* flags;         // [0]: a 64-token tile's log-decay left the fast path's exponent domain
+  int* flags;         // [h * nseg]: per forward segment-pass CTA, a 64-token tile's log-decay left the
+                      // fast path's exponent domain
 };
 
 // The fused kernels scale q / k by e^{+-(logb - r)} with r the tile's middle row, so a tile whose total
@@ -68,7 +69,7 @@ inline long long ws_bytes(const Plan& p) {
   const long long st = (long long)p.h * p.nseg * D * D * 4;
   const long long vec = (long long)p.h * p.nseg * D * 4;
   const long long sp = (long long)p.h * p.ntiles * STATE_BF16;
-  return 4 * st + 3 * vec + sp + 4096 + 256;
+  return 4 * st + 3 * vec + sp + 4096 + (((long long)p.h * p.nseg * 4 + 255) & ~255ll);
 }
 
 inline Ws carve(const Plan& p, void* base) {

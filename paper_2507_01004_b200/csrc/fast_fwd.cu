@@ -16,6 +16,7 @@
 //   the tile (in-chunk reference point: |exponent| <= |gamma|/2).
 //   The incoming state of every segment already contains the cross-rank
 //   correction e^{G_t} S_prev (fused, no extra pass over HBM).
+#include <vector>
 #include "fast_common.cuh"
 
 namespace zgla {
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
   int t0, t1;
   seg_range(s, nseg, ntiles, t0, t1);
   const int nt = t1 - t0;
+  int bad = 0;  // DIR 0: a tile of this segment left the exponent domain
 
   if (tid == 0) {
     for (int i = 0; i < KS_NS; ++i) {
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
 #pragma unroll
       for (int r = 1; r < 64; ++r) lb[r] += lb[r - 1];
       const float gam = lb[63];
-      if (DIR == 0 && flags != nullptr && !(gam >= -2.f * DOMAIN_EXP)) atomicOr(flags, 1);  // also catches NaN
+      if (DIR == 0 && !(gam >= -2.f * DOMAIN_EXP)) bad = 1;  // also catches NaN
       xg[(i & 3) * D + c] = gam;
       mbar_arrive(&gready[i & 3]);
       if (i >= 1) {  // gamma of tile i-1 (other group)
@@ -177,7 +179,9 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
     if (nt > 0 && grp == ((nt - 1) & 1)) out_gam[(long long)(hh * nseg + s) * D + c] = last_tot;
   }
   tc_fence_before();
-  __syncthreads();
+  // one domain flag word per CTA, written every call: no reset pass is needed before the kernel
+  bad = __syncthreads_or(bad);
+  if (DIR == 0 && flags != nullptr && threadIdx.x == 0) flags[blockIdx.x] = bad;
   if (warp == 9) tmem_dealloc(tbase, 128);
 }
 
@@ -662,7 +666,6 @@ int fast_fwd_local(const zgla_shape* s, int num_sms, const TRef& k, const TRef& 
                    void* s_local, void* g_tot, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
-  if (cudaError_t e = cudaMemsetAsync(w.flags, 0, sizeof(int), st)) return cuda_fail(e, "fast_fwd_local");
   if (int rc = launch_seg_state(0, pl, k, v, g, w.dS, w.gam, w.flags, st)) return rc;
   const long long n = (long long)pl.h * D * D;
   if (cudaError_t e = launch_k(seg_scan_kernel<0>, (unsigned)((n / 4 + 127) / 128), 128, 0, st, pl.h, pl.nseg, k.dr,
@@ -714,9 +717,13 @@ namespace zgla {
 int fast_domain_flag(const zgla_shape* s, int num_sms, const void* ws, int* host_flag, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, const_cast<void*>(ws));
-  if (cudaError_t e = cudaMemcpyAsync(host_flag, w.flags, sizeof(int), cudaMemcpyDeviceToHost, st))
+  std::vector<int> f((size_t)pl.h * pl.nseg);  // one word per forward segment-pass CTA
+  if (cudaError_t e = cudaMemcpyAsync(f.data(), w.flags, f.size() * sizeof(int), cudaMemcpyDeviceToHost, st))
     return cuda_fail(e, "zgla_zeco_domain_check");
   if (cudaError_t e = cudaStreamSynchronize(st)) return cuda_fail(e, "zgla_zeco_domain_check");
+  int any = 0;
+  for (int x : f) any |= x;
+  *host_flag = any;
   return ZGLA_OK;
 }
 }  // namespace zgla
