@@ -159,6 +159,52 @@ def test_fast_deterministic_and_linear_in_v_at_cfg2():
     assert err <= TOL_BF16, err
 
 
+def test_fast_causality_bitwise_at_cfg2():
+    """Full BASELINE config-2 size, exact (bitwise) causality of the segment-parallel kernels.
+    Forward: changing k / v of token t leaves o[:t] and every other head bit-identical.
+    Backward: changing dO of token t leaves dq everywhere but at t, dk / dv after t and dg after t's
+    64-token tile bit-identical (dq_i needs dO_i only; dk_j, dv_j, dg_j need dO_i for i >= j)."""
+    from paper_2507_01004_b200 import ops
+    torch.manual_seed(5)
+    h, L, D, hp = 16, 16384, 128, 5
+    t = 9 * 1024 + 64 * 7 + 17  # inside a tile, inside a segment (not a boundary)
+    sh = ops.ZecoShard(h, L, D, D, 64, torch.bfloat16)
+    q, k, v, do = ((torch.rand(h, L, D, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(4))
+    g = torch.rand(h, L, D, device="cuda") * (math.log(0.999) - math.log(0.9)) + math.log(0.9)
+
+    def step(k, v, do):
+        sh.fwd_local(k, v, g)
+        o = sh.fwd_output(q, k, v, g).clone()
+        sh.bwd_local(q, g, do)
+        return o, [x.clone() for x in sh.bwd_output(q, k, v, g, do, None, None)]
+
+    o0, (dq0, dk0, dv0, dg0) = step(k, v, do)
+    k1, v1 = k.clone(), v.clone()
+    k1[hp, t] = -k1[hp, t]
+    v1[hp, t] = v1[hp, t] * 2 + 0.5
+    o1, _ = step(k1, v1, do)
+    others = [x for x in range(h) if x != hp]
+    assert torch.equal(o1[others], o0[others])
+    assert torch.equal(o1[hp, :t], o0[hp, :t])
+    assert not torch.equal(o1[hp, t:], o0[hp, t:])
+
+    do1 = do.clone()
+    do1[hp, t] = -do1[hp, t] + 0.25
+    _, (dq1, dk1, dv1, dg1) = step(k, v, do1)
+    for a, b in ((dq1, dq0), (dk1, dk0), (dv1, dv0), (dg1, dg0)):
+        assert torch.equal(a[others], b[others])
+    assert torch.equal(dq1[hp, :t], dq0[hp, :t]) and torch.equal(dq1[hp, t + 1:], dq0[hp, t + 1:])
+    for a, b in ((dk1, dk0), (dv1, dv0), (dg1, dg0)):
+        assert not torch.equal(a[hp, :t + 1], b[hp, :t + 1])
+    for a, b in ((dk1, dk0), (dv1, dv0)):
+        assert torch.equal(a[hp, t + 1:], b[hp, t + 1:])
+    # dg inside a tile is the tile's suffix sum taken as (tile total - prefix): bit-identical from the
+    # next tile on, equal up to fp32 rounding between t and the end of its tile
+    te = (t // 64 + 1) * 64
+    assert torch.equal(dg1[hp, te:], dg0[hp, te:])
+    torch.testing.assert_close(dg1[hp, t + 1:te], dg0[hp, t + 1:te], rtol=1e-5, atol=1e-4)
+
+
 @pytest.mark.parametrize("lo,hi", [(math.log(0.5), math.log(0.9)), (math.log(0.2), math.log(0.5))])
 def test_fast_strong_decay_inside_domain(lo, hi):
     """Strong gates (per-token decay down to 0.2: 64-token tile log-decay down to about -103, in-tile
