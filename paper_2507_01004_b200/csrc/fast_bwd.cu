@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_do);
       tma_prefetch_desc(&tm_sp);
+      if (ZGLA_G_PREFETCH) tma_prefetch_desc(&tm_g);
       const uint64_t pol = ZGLA_CONSUMER_EVICT_FIRST ? l2_policy_evict_first() : 0;  // 0: no cache hint
       for (int m = 0; m < nt; ++m) {
         const int st = m % BO_NS, ph = (m / BO_NS) & 1;
@@ -170,6 +171,14 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           mbar_arrive_expect_tx(sp_full, T * 128);
           tma_load_2d(sp_buf, &tm_sp, sp_full, 0, (hh * ntiles + n) * 64);
         }
+#if ZGLA_G_PREFETCH
+        // warm L2 with the gate tile the prep warps read (pointer loads) ZGLA_G_PREFETCH tiles from now
+        if (n - ZGLA_G_PREFETCH >= t0) {
+          const int rg = (n - ZGLA_G_PREFETCH) * T;
+          if (in3d) tma_prefetch_3d(&tm_g, 0, rg, hh);
+          else tma_prefetch_2d(&tm_g, 0, (int)(hh * L + rg));
+        }
+#endif
         ZTRACE(tr, 0, m);
       }
     }

@@ -20,6 +20,12 @@
 #ifndef ZGLA_L2_KEEP_PCT
 #define ZGLA_L2_KEEP_PCT 20  // percent of a producer walk (K1 / K4) loaded with normal L2 priority (tuned: 0.3995 -> 0.3895 ms)
 #endif
+#ifndef ZGLA_G_PREFETCH
+#define ZGLA_G_PREFETCH 1  // bwd: L2 prefetch of the gate tile this many tiles ahead (0: off); 1 tuned (2: worse)
+#endif
+#ifndef ZGLA_G_PREFETCH_FWD
+#define ZGLA_G_PREFETCH_FWD 1  // fwd: L2 prefetch of the gate tile this many tiles ahead (0: off)
+#endif
 #ifndef ZGLA_CONSUMER_EVICT_FIRST
 #define ZGLA_CONSUMER_EVICT_FIRST 0  // consumer kernels (K3 / K6): 1 = evict-first hint, 0 = plain loads
 #endif

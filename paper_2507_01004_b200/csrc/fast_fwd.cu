@@ -351,6 +351,14 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         tile_load<DENSE>(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r, hh, L, in3d, pol);
         tile_load<DENSE>(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r, hh, L, in3d, pol);
         tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d, pol);
+#if ZGLA_G_PREFETCH_FWD
+        // warm L2 with the gate tile the prep warps read (pointer loads) a few tiles from now
+        if (n + ZGLA_G_PREFETCH_FWD < nt) {
+          const int rg = (t0 + n + ZGLA_G_PREFETCH_FWD) * T;
+          if (in3d) tma_prefetch_3d(&tm_g, 0, rg, hh);
+          else tma_prefetch_2d(&tm_g, 0, (int)(hh * L + rg));
+        }
+#endif
         ZTRACE(tr, 0, n);
       }
     }
