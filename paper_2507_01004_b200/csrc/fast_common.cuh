@@ -26,6 +26,9 @@
 #ifndef ZGLA_G_PREFETCH_FWD
 #define ZGLA_G_PREFETCH_FWD 1  // fwd: L2 prefetch of the gate tile this many tiles ahead (0: off)
 #endif
+#ifndef ZGLA_O_TMA
+#define ZGLA_O_TMA 1  // fwd: O through a swizzled staging tile and bulk tensor stores (dense outputs)
+#endif
 #ifndef ZGLA_CONSUMER_EVICT_FIRST
 #define ZGLA_CONSUMER_EVICT_FIRST 0  // consumer kernels (K3 / K6): 1 = evict-first hint, 0 = plain loads
 #endif

@@ -250,7 +250,8 @@ constexpr int FO_STAGE = 3 * TILE_BF16;  // q, k, v = 48 KiB (g goes straight to
 constexpr int FO_THREADS = 448;  // 4 state warps, 8 prep warps (2 groups, alternate tiles), TMA, MMA
 constexpr int FO_OFF_SP = FO_NS * FO_STAGE;         // S' (bf16 [D][D], 2 panels)
 constexpr int FO_OFF_AM = FO_OFF_SP + STATE_BF16;   // masked scores (bf16 [64][64], 1 panel)
-constexpr int FO_OFF_VEC = FO_OFF_AM + T * T * 2;   // gamma / r per stage
+constexpr int FO_OFF_OST = FO_OFF_AM + T * T * 2;   // O staging for the TMA store (2 x [64][128] bf16, 2 panels each)
+constexpr int FO_OFF_VEC = FO_OFF_OST + (ZGLA_O_TMA ? 2 * TILE_BF16 : 0);  // gamma / r per stage
 constexpr int FO_OFF_X = FO_OFF_VEC + FO_NS * 2 * D * 4;
 constexpr int FO_OFF_BAR = FO_OFF_X + 2 * 64 * 8;
 constexpr size_t FO_SMEM = 1024 + FO_OFF_BAR + 256;
@@ -261,7 +262,8 @@ template <bool DENSE>
 __global__ void __launch_bounds__(FO_THREADS, 1)
     fwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g,
-                   const __grid_constant__ CUtensorMap tm_sp, const float* __restrict__ g, long long gts,
+                   const __grid_constant__ CUtensorMap tm_sp, const __grid_constant__ CUtensorMap tm_o,
+                   const float* __restrict__ g, long long gts,
                    long long ghs, long long L, int in3d, int dr, int nseg, int ntiles,
                    const float* __restrict__ Sin,
                    const float* __restrict__ cumG, const float* __restrict__ s_prev,
@@ -272,6 +274,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sp_buf = smem + FO_OFF_SP;
   uint8_t* am_buf = smem + FO_OFF_AM;
+  uint8_t* ostage = smem + FO_OFF_OST;
   float* vgam = reinterpret_cast<float*>(smem + FO_OFF_VEC);  // [NS][D]
   float* vr = vgam + FO_NS * D;                               // [NS][D]
   float2* xa = reinterpret_cast<float2*>(smem + FO_OFF_X);
@@ -613,6 +616,43 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       tc_fence_after();
       if (tid == 0) ZTRACE(tr, 9, n);
       const int ob = n & 1;
+      if constexpr (DENSE && ZGLA_O_TMA) {
+        // rows -> swizzled staging tile (16-byte shared stores), then one bulk tensor store per 64 channels
+        uint8_t* os = ostage + (n & 1) * TILE_BF16;
+        if (tid == 0) tma_store_wait_read1();  // the store of tile n-2 has read this buffer
+        named_bar(3, 128);
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+          if (32 * q >= dr) break;
+          float o[32];
+          tmem_ld32(taddr(tbase, 32 * qd, COL_O + 32 * q), o);
+          if ((lane >> 4) == ob) {
+            const int i = 16 * qd + (lane & 15);
+            uint8_t* pan = os + (q >> 1) * PANEL;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              uint4 w;
+              w.x = pack_bf16(o[8 * m + 0], o[8 * m + 1]);
+              w.y = pack_bf16(o[8 * m + 2], o[8 * m + 3]);
+              w.z = pack_bf16(o[8 * m + 4], o[8 * m + 5]);
+              w.w = pack_bf16(o[8 * m + 6], o[8 * m + 7]);
+              *reinterpret_cast<uint4*>(pan + sw128(i, 4 * (q & 1) + m)) = w;
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&o_empty[ob]);
+        fence_proxy_async();
+        named_bar(3, 128);
+        if (tid == 0) {
+          const int row = (int)(hh * L + (long long)(t0 + n) * T);
+          tma_store_2d(&tm_o, os, 0, row);
+          if (dr == D) tma_store_2d(&tm_o, os + PANEL, 64, row);
+          tma_store_commit();
+        }
+        if (tid == 0) ZTRACE(tr, 10, n);
+        continue;
+      }
 #pragma unroll 1
       for (int q = 0; q < 4; ++q) {
         float o[32];
@@ -635,6 +675,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       mbar_arrive(&o_empty[ob]);
       if (tid == 0) ZTRACE(tr, 10, n);
     }
+    if (DENSE && ZGLA_O_TMA && tid == 0) tma_store_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -696,10 +737,13 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   if (int rc = map_act(&mk, k, pl.L, pl.h, din)) return rc;
   if (int rc = map_act(&mv, v, pl.L, pl.h, din)) return rc;
   if (int rc = map_gate(&mg, g, pl.L, pl.h, din && is_dense(g, pl.L))) return rc;
+  CUtensorMap mo = mq;  // the strided variant stores O through pointers
+  if (dn && ZGLA_O_TMA)
+    if (int rc = map_act(&mo, o, pl.L, pl.h, true)) return rc;
   auto kern = dn ? fwd_out_kernel<true> : fwd_out_kernel<false>;
   set_smem_once((const void*)kern, (int)FO_SMEM);
   if (cudaError_t e = launch_kp(ZGLA_EARLY || pdl_enabled(), kern, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
-                                (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
+                                mo, (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
                                 (const float*)w.Sin, (const float*)w.cumG, (const float*)s_prev, (__nv_bfloat16*)o.p,
                                 o.ts, o.hs, w.Sp,
                                 g_trace_buf, g_trace_cta))
