@@ -29,9 +29,6 @@
 #ifndef ZGLA_O_TMA
 #define ZGLA_O_TMA 1  // fwd: O through a swizzled staging tile and bulk tensor stores (dense outputs)
 #endif
-#ifndef ZGLA_FPREP_PAIRS
-#define ZGLA_FPREP_PAIRS 0  // fwd prep: one thread per channel pair and row half (full-width shared wavefronts)
-#endif
 #ifndef ZGLA_CONSUMER_EVICT_FIRST
 #define ZGLA_CONSUMER_EVICT_FIRST 0  // consumer kernels (K3 / K6): 1 = evict-first hint, 0 = plain loads
 #endif

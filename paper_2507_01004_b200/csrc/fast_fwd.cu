@@ -253,7 +253,7 @@ constexpr int FO_OFF_AM = FO_OFF_SP + STATE_BF16;   // masked scores (bf16 [64][
 constexpr int FO_OFF_OST = FO_OFF_AM + T * T * 2;   // O staging for the TMA store (2 x [64][128] bf16, 2 panels each)
 constexpr int FO_OFF_VEC = FO_OFF_OST + (ZGLA_O_TMA ? 2 * TILE_BF16 : 0);  // gamma / r per stage
 constexpr int FO_OFF_X = FO_OFF_VEC + FO_NS * 2 * D * 4;
-constexpr int FO_OFF_BAR = FO_OFF_X + (ZGLA_FPREP_PAIRS ? 2 * 2 * D * 4 : 2 * 64 * 8);
+constexpr int FO_OFF_BAR = FO_OFF_X + 2 * 64 * 8;
 constexpr size_t FO_SMEM = 1024 + FO_OFF_BAR + 256;
 // TMEM columns
 constexpr uint32_t COL_KV = 0, COL_O = 128, COL_A = 256, COL_S = 320;
@@ -431,85 +431,6 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       if (save_sp) tma_store_wait0();
     }
   } else if (warp >= 4) {
-#if ZGLA_FPREP_PAIRS
-    // ---------------- prep (2 groups of 4 warps, alternate tiles).  Group warp wg covers the 64 channels of
-    //   panel wg & 1 for rows [32h, 32h+32), h = wg >> 1; lane l owns the channel pair (c0, c0 + 1),
-    //   c0 = 64 (wg & 1) + 2 l: every 4-byte shared access of a warp is one whole 128-byte panel row.
-    //   The upper row half continues the lower half's running sum (r = logb[31] through shared memory
-    //   and a group barrier), so logb is the same sequential sum as with one thread per channel.
-    const int t = tid - 128;
-    const int grp = t >> 7, wg = (t >> 5) & 3;
-    const int hr = wg >> 1, c0 = 64 * (wg & 1) + 2 * lane;
-    const uint32_t coff = (wg & 1) * PANEL + 4 * (lane & 3), cchk = lane >> 2;
-    float* rx = reinterpret_cast<float*>(smem + FO_OFF_X) + grp * 2 * D;  // [parity][D] r of this group's tiles
-    constexpr float LOG2E = 1.4426950408889634f;
-    for (int n = grp; n < nt; n += 2) {
-      const int st = n % FO_NS, ph = (n / FO_NS) & 1;
-      uint8_t* sb = smem + st * FO_STAGE;
-      float* rxp = rx + ((n >> 1) & 1) * D;
-      float la[32], lb2[32];  // logb of channels c0, c0 + 1 over this warp's 32 rows
-      const float* gp = g + hh * ghs + ((long long)(t0 + n) * T + 32 * hr) * gts + c0;
-      if (DENSE || c0 < dr) {
-#pragma unroll
-        for (int r = 0; r < 32; ++r) {
-          const float2 x = __ldg(reinterpret_cast<const float2*>(gp + r * gts));
-          la[r] = x.x;
-          lb2[r] = x.y;
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < 32; ++r) la[r] = lb2[r] = 0.f;  // zero-filled channels of a d = 64 head
-      }
-      float ra, rb;
-      if (hr == 0) {
-#pragma unroll
-        for (int r = 1; r < 32; ++r) la[r] += la[r - 1], lb2[r] += lb2[r - 1];
-        ra = la[31], rb = lb2[31];
-        *reinterpret_cast<float2*>(rxp + c0) = make_float2(ra, rb);
-        named_bar(1 + grp, 128);
-      } else {
-        named_bar(1 + grp, 128);
-        const float2 rr2 = *reinterpret_cast<const float2*>(rxp + c0);
-        ra = rr2.x, rb = rr2.y;
-        la[0] += ra, lb2[0] += rb;
-#pragma unroll
-        for (int r = 1; r < 32; ++r) la[r] += la[r - 1], lb2[r] += lb2[r - 1];
-      }
-      mbar_wait(&full[st], ph);
-      if (t == 0 || t == 128) ZTRACE(tr, 12, n);
-      if (hr == 1) {
-        *reinterpret_cast<float2*>(vgam + st * D + c0) = make_float2(la[31], lb2[31]);
-      } else {
-        *reinterpret_cast<float2*>(vr + st * D + c0) = make_float2(ra, rb);
-      }
-#pragma unroll
-      for (int k0 = 0; k0 < 32; k0 += 8) {  // batches: all loads, then all stores (smem may alias)
-        uint32_t xq[8], xk[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t o = coff + sw128(32 * hr + k0 + k, cchk);
-          xq[k] = *reinterpret_cast<const uint32_t*>(sb + o);
-          xk[k] = *reinterpret_cast<const uint32_t*>(sb + TILE_BF16 + o);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float da = (la[k0 + k] - ra) * LOG2E, db = (lb2[k0 + k] - rb) * LOG2E;
-          const float2 q2 = unpack_bf16(xq[k]), k2 = unpack_bf16(xk[k]);
-          xq[k] = pack_bf16(q2.x * fast_exp2(da), q2.y * fast_exp2(db));
-          xk[k] = pack_bf16(k2.x * fast_exp2(-da), k2.y * fast_exp2(-db));
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t o = coff + sw128(32 * hr + k0 + k, cchk);
-          *reinterpret_cast<uint32_t*>(sb + o) = xq[k];
-          *reinterpret_cast<uint32_t*>(sb + TILE_BF16 + o) = xk[k];
-        }
-      }
-      fence_proxy_async();
-      mbar_arrive(&prep[st]);
-      if (t == 0 || t == 128) ZTRACE(tr, 1, n);
-    }
-#else
     // ---------------- prep (2 groups of 4 warps, alternate tiles): one thread per channel c:
     //                  in-chunk log cumsum over the 64 rows, r = logb[31], gamma = logb[63], Qh / Kh in place
     const int t = tid - 128;
@@ -565,7 +486,6 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       mbar_arrive(&prep[st]);
       if (t == 0 || t == 128) ZTRACE(tr, 1, n);
     }
-#endif
   } else {
     // ---------------- state / epilogue warps (4): thread owns row c of the fp32 state S (in TMEM)
     const int qd = warp;
