@@ -207,7 +207,7 @@ __device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
 template <int DIR>
 __global__ void seg_scan_kernel(int h, int nseg, int dr, const float* __restrict__ dS, const float* __restrict__ gam,
                                 float* __restrict__ Sin, float* __restrict__ cumG, float* __restrict__ s_local,
-                                float* __restrict__ g_tot) {
+                                float* __restrict__ g_tot, const float* __restrict__ pf0, const float* __restrict__ pf1) {
   pdl_wait();
   pdl_trigger();
   const long long idx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
@@ -223,6 +223,11 @@ __global__ void seg_scan_kernel(int h, int nseg, int dr, const float* __restrict
       const int s = DIR == 0 ? b0 + j : nseg - 1 - b0 - j;
       const bool ok = b0 + j < nseg;
       x[j] = ok ? __ldcs(reinterpret_cast<const float4*>(dS + base + (long long)s * D * D)) : make_float4(0, 0, 0, 0);
+      // K5: warm L2 with the forward segment states the backward output kernel's prologue reads next
+      if (DIR == 1 && pf0 != nullptr && ok && (threadIdx.x & 7) == 0) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pf0 + base + (long long)s * D * D));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pf1 + base + (long long)s * D * D));
+      }
       gg[j] = ok ? __ldg(reinterpret_cast<const float4*>(gm + s * D)) : make_float4(0, 0, 0, 0);
     }
 #pragma unroll
@@ -718,7 +723,8 @@ int fast_fwd_local(const zgla_shape* s, int num_sms, const TRef& k, const TRef& 
   if (int rc = launch_seg_state(0, pl, k, v, g, w.dS, w.gam, w.flags, st)) return rc;
   const long long n = (long long)pl.h * D * D;
   if (cudaError_t e = launch_k(seg_scan_kernel<0>, (unsigned)((n / 4 + 127) / 128), 128, 0, st, pl.h, pl.nseg, k.dr,
-                                (const float*)w.dS, (const float*)w.gam, w.Sin, w.cumG, (float*)s_local, (float*)g_tot))
+                                (const float*)w.dS, (const float*)w.gam, w.Sin, w.cumG, (float*)s_local, (float*)g_tot,
+                                (const float*)nullptr, (const float*)nullptr))
     return cuda_fail(e, "seg_scan_kernel<0>");
   return zgla_check_launch();
 }
@@ -758,7 +764,8 @@ int fast_bwd_local(const zgla_shape* s, int num_sms, const TRef& q, const TRef& 
   if (int rc = launch_seg_state(1, pl, q, d_out, g, w.dD, w.gam, nullptr, st)) return rc;
   const long long n = (long long)pl.h * D * D;
   if (cudaError_t e = launch_k(seg_scan_kernel<1>, (unsigned)((n / 4 + 127) / 128), 128, 0, st, pl.h, pl.nseg, q.dr,
-                                (const float*)w.dD, (const float*)w.gam, w.Dend, w.cumGr, (float*)ds0, (float*)nullptr))
+                                (const float*)w.dD, (const float*)w.gam, w.Dend, w.cumGr, (float*)ds0, (float*)nullptr,
+                                (const float*)w.Sin, (const float*)w.dS))
     return cuda_fail(e, "seg_scan_kernel<1>");
   return zgla_check_launch();
 }
