@@ -95,3 +95,17 @@ def test_plain_c_client_compiles_and_links(tmp_path):
                     "-L", lib, "-lzeco_gla", f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
     assert out.startswith("zeco-gla-b200")
+
+
+def test_integration_ctypes_stub_matches_header():
+    """The ctypes binding shown in INTEGRATION.md declares the same arity as include/zeco_gla.h."""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    header = open(os.path.join(root, "include", "zeco_gla.h")).read()
+    doc = open(os.path.join(root, "INTEGRATION.md")).read()
+    stub = re.findall(r'"(zgla_\w+)":\s*\[ctypes\.POINTER\(_Shape\), ctypes\.c_int\](?:\s*\+\s*\[_V\]\s*\*\s*(\d+))?', doc)
+    assert len(stub) >= 5
+    for name, n in stub:
+        m = re.search(r"\b" + name + r"\s*\(([^;]*?)\)\s*;", header, re.S)
+        assert m, name
+        assert len(m.group(1).split(",")) == 2 + int(n or 0), name
