@@ -66,8 +66,6 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   uint8_t* dpm_buf = smem + BO_OFF_DPM;
   float* vgam = reinterpret_cast<float*>(smem + BO_OFF_VEC);
   float* vr = vgam + BO_NS * D;
-  float2* xa = reinterpret_cast<float2*>(smem + BO_OFF_X);  // prep exchange (64 + 64 float2)
-  float2* xb = xa + 64;
   float* xrho = reinterpret_cast<float*>(smem + BO_OFF_X + 1024);  // [2][D] row-sum partials
   float* xtot = xrho + 2 * D;                                      // [D] logb of row 31 (epilogue)
   float* xcarry = xtot + D;                                        // [2][D] per-half sums of da
@@ -262,8 +260,8 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       uint8_t* sb = smem + st * BO_STAGE;
       float lb[64];
       const float* gp = g + hh * ghs + (long long)n * T * gts + c;
-#pragma unroll
       if constexpr (DENSE) {
+#pragma unroll
         for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);  // immediate offsets
       } else if (c < dr) {
         const float* pr = gp;  // runtime stride: one pointer bump per row keeps the loads back to back
@@ -276,12 +274,13 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
 #pragma unroll
       for (int r = 1; r < 64; ++r) lb[r] += lb[r - 1];
       const float rr = lb[31];
+      const float gam = (lb[63] - rr) + rr;  // (same rounding as the unscaled walk)
 #pragma unroll
-      for (int r = 0; r < 64; ++r) lb[r] -= rr;
+      for (int r = 0; r < 64; ++r) lb[r] = (lb[r] - rr) * LOG2E;  // log2-scaled d: TMEM holds it for the epilogue
       if (c == 0) ZTRACE(tr, 10, m);
       mbar_wait(&full[st], ph);
       if (c == 0) ZTRACE(tr, 11, m);
-      vgam[st * D + c] = lb[63] + rr;
+      vgam[st * D + c] = gam;
       vr[st * D + c] = rr;
 #pragma unroll
       for (int r0 = 0; r0 < 64; r0 += 8) {  // batches: all loads, then all stores (smem may alias)
@@ -294,7 +293,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         }
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          const float d = lb[r0 + r] * LOG2E;
+          const float d = lb[r0 + r];
           xq[r] = __float2bfloat16_rn(__bfloat162float(xq[r]) * fast_exp2(d));
           xk[r] = __float2bfloat16_rn(__bfloat162float(xk[r]) * fast_exp2(-d));
         }
@@ -441,7 +440,6 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const uint32_t cols = 32 * ch;
       const uint32_t lbcol = BC_LB + 64 * (m & 1) + cols;
       const long long tok0 = (long long)n * T + cols;  // token index inside the head
-      constexpr float LOG2E = 1.4426950408889634f;
       float da[32];
       float tsum = 0.f;
       __nv_bfloat16* pdq = dq + hh * gs.qh + tok0 * gs.qt + c;
@@ -468,7 +466,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         for (int u = 0; u < 8; ++u) {
           const int i = 8 * h8 + u;
           const float q_raw = __uint_as_float(gq[u]), k_raw = __uint_as_float(gk[u]);
-          const float dlt = __uint_as_float(dl[u]) * LOG2E;
+          const float dlt = __uint_as_float(dl[u]);  // (logb - r) * log2(e), from the prep warps
           da[i] = __fsub_rn(__fmul_rn(qh[u], q_raw), __fmul_rn(kh[u], k_raw));  // no FMA contraction: identical in every variant
           tsum += da[i];
           if (DENSE || c < dr) {  // channels of a d = 64 head beyond 64 are padding

@@ -282,8 +282,6 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   uint8_t* ostage = smem + FO_OFF_OST;
   float* vgam = reinterpret_cast<float*>(smem + FO_OFF_VEC);  // [NS][D]
   float* vr = vgam + FO_NS * D;                               // [NS][D]
-  float2* xa = reinterpret_cast<float2*>(smem + FO_OFF_X);
-  float2* xb = xa + 64;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FO_OFF_BAR);
   uint64_t* full = bars;
   uint64_t* empty = bars + FO_NS;
@@ -447,8 +445,8 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       uint8_t* sb = smem + st * FO_STAGE;
       float lb[64];
       const float* gp = g + hh * ghs + (long long)(t0 + n) * T * gts + c;
-#pragma unroll
       if constexpr (DENSE) {
+#pragma unroll
         for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);  // immediate offsets
       } else if (c < dr) {
         const float* pr = gp;  // runtime stride: one pointer bump per row keeps the loads back to back
@@ -655,29 +653,28 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
           if (dr == D) tma_store_2d(&tm_o, os + PANEL, 64, row);
           tma_store_commit();
         }
-        if (tid == 0) ZTRACE(tr, 10, n);
-        continue;
-      }
+      } else {  // strided / d = 64 outputs: 16-byte row pieces straight from the lane half that holds them
 #pragma unroll 1
-      for (int q = 0; q < 4; ++q) {
-        float o[32];
-        tmem_ld32(taddr(tbase, 32 * qd, COL_O + 32 * q), o);
-        if ((lane >> 4) == ob && 32 * q < dr) {
-          const int i = 16 * qd + (lane & 15);
-          uint4* dst = reinterpret_cast<uint4*>(out + hh * ohs + ((long long)(t0 + n) * T + i) * ots + 32 * q);
+        for (int q = 0; q < 4; ++q) {
+          float o[32];
+          tmem_ld32(taddr(tbase, 32 * qd, COL_O + 32 * q), o);
+          if ((lane >> 4) == ob && 32 * q < dr) {
+            const int i = 16 * qd + (lane & 15);
+            uint4* dst = reinterpret_cast<uint4*>(out + hh * ohs + ((long long)(t0 + n) * T + i) * ots + 32 * q);
 #pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            uint4 w;
-            w.x = pack_bf16(o[8 * m + 0], o[8 * m + 1]);
-            w.y = pack_bf16(o[8 * m + 2], o[8 * m + 3]);
-            w.z = pack_bf16(o[8 * m + 4], o[8 * m + 5]);
-            w.w = pack_bf16(o[8 * m + 6], o[8 * m + 7]);
-            dst[m] = w;
+            for (int m = 0; m < 4; ++m) {
+              uint4 w;
+              w.x = pack_bf16(o[8 * m + 0], o[8 * m + 1]);
+              w.y = pack_bf16(o[8 * m + 2], o[8 * m + 3]);
+              w.z = pack_bf16(o[8 * m + 4], o[8 * m + 5]);
+              w.w = pack_bf16(o[8 * m + 6], o[8 * m + 7]);
+              dst[m] = w;
+            }
           }
         }
+        tc_fence_before();
+        mbar_arrive(&o_empty[ob]);
       }
-      tc_fence_before();
-      mbar_arrive(&o_empty[ob]);
       if (tid == 0) ZTRACE(tr, 10, n);
     }
     if (DENSE && ZGLA_O_TMA && tid == 0) tma_store_wait0();
