@@ -130,9 +130,14 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  // only the epilogue warps' prologue reads the preceding scan's outputs (Dend, cumGr)
+  // under a programmatic (PDL) launch every warp waits for the preceding grid before touching memory;
+  // ZGLA_EARLY: only the epilogue warps, whose prologue reads the preceding scan's outputs (Dend, cumGr)
   pdl_trigger();
-  if (warp < 8) pdl_wait();
+#if ZGLA_EARLY
+  if (warp < 8) pdl_wait();  // the other warps stream inputs the preceding kernel did not write
+#else
+  pdl_wait();
+#endif
 
   if (warp == 12) {
     // ---------------- TMA producer (tiles right to left)

@@ -278,14 +278,15 @@ inline void set_smem_once(const void* fn, int bytes) {
 
 // ---- launches with programmatic dependent launch (PDL): a kernel's CTAs become resident as the
 // previous kernel's CTAs retire and run their prologue (barrier init, TMEM alloc, descriptor
-// prefetch) before griddepcontrol.wait releases them.  Every fused kernel waits before its first
-// global access and triggers its dependents only after that wait, so when kernel X+1 starts, X-1
-// has completed.  Opt-in (ZGLA_PDL=1): measured on cfg2 it shortens eager launches by ~2 us per
-// kernel pair but lengthens the CUDA-graph step (0.3945 -> 0.400 ms), so graphs launch plainly.
+// prefetch) before griddepcontrol.wait releases them.  Every warp of every fused kernel waits before
+// its first global access (unless compiled with ZGLA_EARLY), and a grid completes only after its own
+// wait, so all memory of the kernels before it is visible.  On by default (ZGLA_PDL=0 turns it off):
+// on the final kernels the CUDA-graph step is 0.3649-0.3660 -> 0.3630-0.3637 ms (round-1 kernels:
+// 0.3945 -> 0.400, then it was opt-in).
 inline bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("ZGLA_PDL");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
 }

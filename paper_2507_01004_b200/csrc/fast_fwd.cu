@@ -335,7 +335,11 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   // Only the state warps read the preceding scan's outputs (Sin, cumG): with an early launch the
   // loads of q / k / v / g and the per-tile prep run while that kernel is still finishing.
   pdl_trigger();
-  if (warp < 4) pdl_wait();
+#if ZGLA_EARLY
+  if (warp < 4) pdl_wait();  // the other warps stream inputs the preceding kernel did not write
+#else
+  pdl_wait();
+#endif
 
   if (warp == 12) {
     // ---------------- TMA producer
