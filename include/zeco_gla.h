@@ -138,6 +138,9 @@ int zgla_zeco_bwd_output_v(const zgla_shape* s, int num_sms, const zgla_tensor* 
 int zgla_allscan_local(int P, int heads, int key_dim, int value_dim, int dtype, int num_blocks, int direction,
                        const void* local_states, const void* log_decays, void* recv, void* scanned,
                        void* stream);
+/* Frees the device scratch zgla_allscan_local keeps between calls (the Python layer calls it at
+ * interpreter exit; the next zgla_allscan_local allocates again). */
+int zgla_release_cached(void);
 
 /* SPMD form over peer memory (one process per GPU).  The caller exchanges the
  * buffers returned by zgla_allscan_export() (CUDA IPC handles) and passes the

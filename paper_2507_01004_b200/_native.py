@@ -7,6 +7,7 @@ raises immediately.
 
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 import threading
@@ -75,6 +76,7 @@ _SIGS = {
     "zgla_zeco_bwd_local_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _P, _P, _P], _I),
     "zgla_zeco_bwd_output_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _T, _T, _P, _P, _P, _T, _T, _T, _T, _P], _I),
     "zgla_allscan_local": ([_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P], _I),
+    "zgla_release_cached": ([], _I),
     "zgla_allscan_create": ([_I, _I, _I, _I, _I, _I, ctypes.POINTER(_P)], _I),
     "zgla_allscan_export": ([_P, _P], _I),
     "zgla_allscan_bind": ([_P, _P, _P], _I),
@@ -115,7 +117,17 @@ def load(path: str | None = None):
                 fn.argtypes = args
                 fn.restype = res
             _lib = lib
+            atexit.register(_release_at_exit)
     return _lib
+
+
+def _release_at_exit():
+    """Free the library's cached device scratch while the CUDA context is still alive."""
+    try:
+        if _lib is not None:
+            _lib.zgla_release_cached()
+    except Exception:  # interpreter teardown: nothing useful to report
+        pass
 
 
 def check(rc: int, what: str) -> None:

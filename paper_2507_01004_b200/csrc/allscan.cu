@@ -292,6 +292,17 @@ extern "C" int zgla_allscan_local(int P, int heads, int key_dim, int value_dim, 
   return zgla_check_launch();
 }
 
+extern "C" int zgla_release_cached(void) {
+  std::lock_guard<std::mutex> lock(g_scratch.mu);
+  if (g_scratch.flags) {
+    cudaError_t e = cudaFree(g_scratch.flags);
+    g_scratch.flags = nullptr;
+    g_scratch.bytes = 0;
+    if (e != cudaSuccess) return cuda_fail(e, "zgla_release_cached");
+  }
+  return ZGLA_OK;
+}
+
 // ------------------------------------------------------------------ SPMD comm
 struct zgla_allscan_comm {
   int rank, world, h, dk, dv, max_blocks;
