@@ -118,6 +118,12 @@ int zgla_zeco_bwd_output(const zgla_shape* s, int num_sms, const void* q, const 
  * synchronises `stream` (a validation call, not for the timed path).  ZGLA_OK on the SIMT paths. */
 int zgla_zeco_domain_check(const zgla_shape* s, int num_sms, const void* ws, void* stream);
 
+/* lazy (non-synchronising) domain report for the timed path: registers a host-mapped int for the
+ * workspace `ws`; every later fused zgla_zeco_fwd_local on that workspace stores 1 into it when a
+ * tile left the exponent domain (no store otherwise).  The caller reads / resets *host_flag whenever
+ * it likes (e.g. at the next step) and raises DomainError.  unwatch frees the word. */
+int zgla_zeco_watch_domain(void* ws, int** host_flag);
+int zgla_zeco_unwatch_domain(void* ws);
 /* the same four entry points over strided tensors (zgla_tensor); ZGLA_ERR_LAYOUT if a stride or base is
  * not 16-byte aligned, or if the shape runs the SIMT path and a tensor is not dense */
 int zgla_zeco_fwd_local_v(const zgla_shape* s, int num_sms, const zgla_tensor* k, const zgla_tensor* v,
@@ -155,6 +161,10 @@ int zgla_allscan_bind_local(zgla_allscan_comm* c, zgla_allscan_comm* next, zgla_
 int zgla_allscan_run(zgla_allscan_comm* c, int num_blocks, int direction, const float* local_state,
                      const float* log_decay, float* recv, float* scanned, void* stream);
 int zgla_allscan_destroy(zgla_allscan_comm* c);
+/* ZGLA_ERR_DEADLOCK if an earlier zgla_allscan_run on this communicator timed out waiting for a
+ * peer (the kernel records it in host-mapped memory and exits instead of trapping); sync != 0 first
+ * synchronises the device so the last call is included.  A timed-out communicator stays unusable. */
+int zgla_allscan_status(zgla_allscan_comm* c, int sync);
 long long zgla_allscan_bytes_sent(const zgla_allscan_comm* c);
 /* rank, world size and head count the communicator was created with (any pointer may be NULL) */
 int zgla_allscan_info(const zgla_allscan_comm* c, int* rank, int* world, int* heads);

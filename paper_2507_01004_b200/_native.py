@@ -71,6 +71,8 @@ _SIGS = {
     "zgla_zeco_bwd_local": ([ctypes.POINTER(Shape), _I, _P, _P, _P, _P, _P, _P], _I),
     "zgla_zeco_bwd_output": ([ctypes.POINTER(Shape), _I] + [_P] * 13, _I),
     "zgla_zeco_domain_check": ([ctypes.POINTER(Shape), _I, _P, _P], _I),
+    "zgla_zeco_watch_domain": ([_P, ctypes.POINTER(ctypes.POINTER(ctypes.c_int))], _I),
+    "zgla_zeco_unwatch_domain": ([_P], _I),
     "zgla_zeco_fwd_local_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _P, _P, _P, _P], _I),
     "zgla_zeco_fwd_output_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _T, _P, _P, _T, _P], _I),
     "zgla_zeco_bwd_local_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _P, _P, _P], _I),
@@ -83,6 +85,7 @@ _SIGS = {
     "zgla_allscan_bind_local": ([_P, _P, _P], _I),
     "zgla_allscan_run": ([_P, _I, _I, _P, _P, _P, _P, _P], _I),
     "zgla_allscan_destroy": ([_P], _I),
+    "zgla_allscan_status": ([_P, _I], _I),
     "zgla_allscan_bytes_sent": ([_P], _LL),
     "zgla_allscan_info": ([_P, _P, _P, _P], _I),
     "zgla_zeco_fwd_bwd_host_bytes": ([ctypes.POINTER(Shape), _I, _I], _LL),

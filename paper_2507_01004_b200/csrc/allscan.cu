@@ -1,26 +1,33 @@
 // All-Scan (paper Alg. 2; reference glasp/collectives.py:70-140) as an in-kernel
-// pipelined chain over peer memory.
+// pipelined chain over peer memory, with a low-latency (LL) data+flag protocol.
 //
-// Every rank owns, per direction, an INBOX (one state, fp32 [h][dk][dv]), a
-// FLAGS array and an ACK array ([K pipeline blocks][B CTAs] u32 each).  Rank
-// p's kernel, for every pipeline block b (rows [b*dk/K, (b+1)*dk/K) of all
-// heads) and for its slice of that block:
-//   1. waits until FLAGS[b][cta] >= epoch (predecessor's data has landed),
-//   2. computes  scanned = e^{G_p} (.) recv + local  (recv = inbox, 0 at the source),
-//   3. stores scanned straight into the SUCCESSOR's inbox (NVLink P2P store
-//      when the successor is another GPU) and, after a system-scope fence,
-//      publishes FLAGS[b][cta] = epoch in the successor's memory,
-//   4. acks consumption of its own inbox block to the predecessor.
-// A producer only overwrites a successor inbox block once that block's ACK
-// from the previous epoch has arrived, so back-to-back calls are safe.  Blocks
-// pipeline exactly as in the reference: rank p forwards block b while block
-// b+1 is still in flight, giving the (K+P-1) hop schedule of Eq. 13.
+// Every word that travels between two ranks is 16 bytes {data, flag, data, flag}:
+// each 8-byte half is written atomically by one vector store, so a receiver that
+// sees flag == epoch in both halves also sees the data next to it.  There is no
+// separate flag store, no fence and no per-block barrier on the data path: every
+// thread of rank p polls its own inbox words, computes
+//     scanned = e^{G_p} (.) recv + local          (recv = 0 at the chain source)
+// and stores the result (with the epoch in both flag slots) straight into the
+// successor's inbox (an NVLink P2P store when the successor is another GPU).
+// The reference's K pipeline blocks (rows [b*dk/K, (b+1)*dk/K) of every head) set
+// the ORDER in which a CTA forwards its words, so block 0 of every CTA leaves
+// first; with LL the pipeline is per word, which is the limit of Eq. 13's
+// (K + P - 1) hop schedule as K grows.  Results are elementwise, so they are
+// bit-identical for every K and every CTA split (tests/test_collectives.py:88-103).
 //
-// The same device code runs the reference's list form (all P ranks resident on
-// one GPU, zgla_allscan_local / zgla_allscan_bind_local) and the SPMD form
-// (one process per GPU, peers mapped with CUDA IPC).  Results are elementwise
-// and independent of K and of the CTA split, so they are bit-identical for
-// every K (reference tests/test_collectives.py:88-103).
+// Inboxes are double-buffered by epoch parity, so a producer only has to know that
+// its successor finished the call TWO epochs back before it overwrites a buffer:
+// one ACK word per direction, published by the successor's last departing CTA, and
+// checked once per CTA at entry (never on the critical path in steady state).
+//
+// A wait that does not complete within the communicator's timeout sets an error
+// word in host-mapped memory and the kernel exits (no trap): the CUDA context
+// stays usable and the next zgla_allscan_run / zgla_allscan_status returns
+// ZGLA_ERR_DEADLOCK (-> DeadlockError, glasp/errors.py).
+//
+// The same device code runs the reference's list form (all P ranks resident on one
+// GPU, zgla_allscan_local) and the SPMD form (one process per GPU, peers mapped with
+// CUDA IPC, or in-process ranks bound with zgla_allscan_bind_local).
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -31,45 +38,44 @@
 namespace zgla {
 namespace allscan {
 
-constexpr int kThreads = 256;
-constexpr int kCtasPerRank = 8;
+constexpr int kThreads = 128;       // light CTAs: they co-reside with the fused kernels (PDL overlap)
+constexpr int kMaxCtas = 256;       // per rank (SPMD); the list form caps P x CTAs at kMaxListCtas
+#ifndef ZGLA_AS_LIST_CAP
+#define ZGLA_AS_LIST_CAP 1024
+#endif
+#ifndef ZGLA_AS_WPT
+#define ZGLA_AS_WPT 4
+#endif
+constexpr int kMaxListCtas = ZGLA_AS_LIST_CAP;
+constexpr int kWordsPerThread = ZGLA_AS_WPT;  // CTA count: ~this many 16-byte words per thread and call (list form;
+                                    // the SPMD form uses half, it has a GPU to itself)
+#ifndef ZGLA_AS_BATCH
+#define ZGLA_AS_BATCH 1
+#endif
+// Words a thread has in flight per step.  Measured (virtual ranks, P = 8, 1 MiB, graph-timed): 1 word
+// 14.0 us, 2: 16.3, 4: 18.4, 8: 24.4 -- every strong (volatile) store of a batch sits between a word's
+// arrival and its departure, so small batches forward sooner; the loads of the next step are the cost.
+constexpr int kBatchList = ZGLA_AS_BATCH;  // list form
+constexpr int kBatchRank = ZGLA_AS_BATCH;  // SPMD form (<= 64 registers: a CTA fits beside a fused-kernel CTA)
 
-template <typename T>
-struct Link {
-  const T* local;
-  const T* logdecay;
-  const T* inbox;         // my incoming buffer (nullptr at the source)
-  const unsigned* flags;  // my incoming flags
-  unsigned* ack_to_pred;  // predecessor's ACK array (peer), nullptr at the source
-  T* succ_inbox;          // successor's inbox (peer), nullptr at the sink
-  unsigned* succ_flags;   // successor's flags (peer)
-  const unsigned* my_ack; // ACKs written by my successor
-  T* recv_out;
-  T* scanned_out;
-};
-
-template <typename T>
-struct V4 {
-  T x, y, z, w;
-};
-__device__ __forceinline__ V4<float> ldcg4(const V4<float>* p) {
-  const float4 v = __ldcg(reinterpret_cast<const float4*>(p));
-  return {v.x, v.y, v.z, v.w};
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
-__device__ __forceinline__ V4<double> ldcg4(const V4<double>* p) {
-  const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
-  const double2 b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
-  return {a.x, a.y, b.x, b.y};
+// LL word accesses: volatile (relaxed.sys / relaxed.gpu / weak stores measured the same)
+__device__ __forceinline__ uint4 ld_volatile4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
 }
-__device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }
-__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
-__device__ __forceinline__ float scan_update(float gl, float r, float x) {
-  return __fadd_rn(__fmul_rn(expf(gl), r), x);
+__device__ __forceinline__ void st_volatile4(uint4* p, uint4 v) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
 }
-__device__ __forceinline__ double scan_update(double gl, double r, double x) {
-  return __dadd_rn(__dmul_rn(exp(gl), r), x);
-}
-
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -78,180 +84,253 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-
-template <bool SYS>
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
-  unsigned v;
-  if (SYS) asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  else asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-template <bool SYS>
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-  if (SYS) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-  else asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-template <bool SYS>
-__device__ __forceinline__ void fence_acq_rel() {
-  if (SYS) asm volatile("fence.acq_rel.sys;" ::: "memory");
-  else asm volatile("fence.acq_rel.gpu;" ::: "memory");
-}
-__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
-
-// poll with relaxed loads; one acquire fence once the value is seen (bar.sync then publishes it to the CTA)
-template <bool SYS>
-__device__ __forceinline__ bool spin_until_geq(const unsigned* p, unsigned target) {
-  long long t0 = clock64();
-  while ((int)(ld_relaxed<SYS>(p) - target) < 0) {
-    if (clock64() - t0 > (1ll << 34)) return false;  // ~8 s at 2 GHz: treat as deadlock
+// scanned = e^{G} * recv + local with the reference's rounding sequence (multiply, then add; no FMA)
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+// EPW consecutive elements of word f (one vector store when EPW = 2)
+template <typename T, int EPW>
+__device__ __forceinline__ void store_el(T* p, int f, const T (&v)[EPW]) {
+  if (p == nullptr) return;
+  if constexpr (EPW == 2 && sizeof(T) == 4) {
+    *reinterpret_cast<float2*>(p + 2 * f) = make_float2(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < EPW; ++k) p[f * EPW + k] = v[k];
   }
-  fence_acq_rel<SYS>();
+}
+
+// element <-> LL word.  fp32: EPW = 2 elements per word {d0, f, d1, f}, or 1 ({d0, f, 0, f}) when a
+// head's block length is odd; fp64: EPW = 1, the two 32-bit halves of the value in the two data slots.
+template <typename T, int EPW>
+struct Word;
+template <int EPW>
+struct Word<float, EPW> {
+  __device__ static uint4 pack(const float (&s)[EPW], unsigned f) {
+    return make_uint4(__float_as_uint(s[0]), f, EPW == 2 ? __float_as_uint(s[EPW - 1]) : 0u, f);
+  }
+  __device__ static void unpack(uint4 w, float (&r)[EPW]) {
+    r[0] = __uint_as_float(w.x);
+    if (EPW == 2) r[EPW - 1] = __uint_as_float(w.z);
+  }
+};
+template <>
+struct Word<double, 1> {
+  __device__ static uint4 pack(const double (&s)[1], unsigned f) {
+    return make_uint4((unsigned)__double2loint(s[0]), f, (unsigned)__double2hiint(s[0]), f);
+  }
+  __device__ static void unpack(uint4 w, double (&r)[1]) { r[0] = __hiloint2double((int)w.z, (int)w.x); }
+};
+
+template <typename T>
+struct Chain {
+  const T* local;
+  const T* logdecay;
+  const uint4* inbox;  // my incoming words (this epoch's parity buffer); nullptr at the source
+  uint4* succ_inbox;   // successor's incoming words (peer memory); nullptr at the sink
+  T* recv_out;
+  T* scanned_out;
+};
+
+// one CTA's share of one rank's chain; false if a wait timed out.  With LL words the pipeline is per
+// word: a word leaves as soon as its predecessor word has arrived, which is the fine-grained limit of
+// the reference's K-block pipelining (glasp/collectives.py:96-131), so K does not change the schedule
+// (nor, the update being elementwise, a single bit of the result).  CTA `cta` owns the contiguous word
+// range [lo, hi) in element order; a thread's kBatch words are all in flight at once.
+template <typename T, int EPW, int kBatch>
+__device__ bool chain_slice(const Chain<T>& A, int nwords, int dv, int cta, int nctas, unsigned epoch,
+                            unsigned long long deadline, unsigned long long* tr = nullptr) {
+  const int per = (nwords + nctas - 1) / nctas;
+  const int lo = min(nwords, cta * per), hi = min(nwords, lo + per);
+  for (int f0 = lo + threadIdx.x; f0 < hi; f0 += kBatch * blockDim.x) {
+    uint4 w[kBatch];
+    T x[kBatch][EPW], eg[kBatch][EPW];
+    // everything that does not depend on the predecessor first: the inbox loads, the local state and
+    // e^{G} (so that only one multiply-add and the stores sit between arrival and departure of a word)
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int f = f0 + j * blockDim.x;
+      w[j] = make_uint4(0, epoch, 0, epoch);
+      if (f < hi) {
+        if (A.inbox) w[j] = ld_volatile4(A.inbox + f);
+#pragma unroll
+        for (int k = 0; k < EPW; ++k) {
+          const int e = f * EPW + k;
+          eg[j][k] = A.logdecay[e / dv];  // [h][dk] decay of state row (head, channel) = e / dv
+          x[j][k] = A.local[e];
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j)
+#pragma unroll
+      for (int k = 0; k < EPW; ++k) eg[j][k] = ex(eg[j][k]);
+    if (A.inbox) {  // poll until every word of the batch carries this epoch in both halves
+      unsigned spins = 0;
+      for (;;) {
+        bool pending = false;
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+          if (w[j].y != epoch || w[j].w != epoch) {
+            pending = true;
+            w[j] = ld_volatile4(A.inbox + f0 + j * blockDim.x);
+          }
+        }
+        if (!pending) break;
+        if ((++spins & 1023u) == 0 && gtimer() > deadline) return false;
+      }
+    }
+    if (tr != nullptr && threadIdx.x == 0 && f0 == lo) tr[1] = gtimer();
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int f = f0 + j * (int)blockDim.x;
+      if (f >= hi) break;
+      T r[EPW], sc[EPW];
+      if (A.inbox) {
+        Word<T, EPW>::unpack(w[j], r);
+      } else {
+#pragma unroll
+        for (int k = 0; k < EPW; ++k) r[k] = T(0);
+      }
+#pragma unroll
+      for (int k = 0; k < EPW; ++k) sc[k] = add_rn(mul_rn(eg[j][k], r[k]), x[j][k]);  // reference rounding
+      if (A.succ_inbox) st_volatile4(A.succ_inbox + f, Word<T, EPW>::pack(sc, epoch));
+      store_el<T, EPW>(A.recv_out, f, r);
+      store_el<T, EPW>(A.scanned_out, f, sc);
+    }
+    if (tr != nullptr && threadIdx.x == 0 && f0 == lo) tr[2] = gtimer();
+  }
   return true;
 }
 
-// one CTA's share of the chain for one rank
-template <typename T, bool SYS>
-__device__ void rank_body(const Link<T>& L, int h, int dk, int dv, int K, int cta, int nctas, unsigned epoch,
-                          int* err) {
-  const int rows = dk / K;
-  const int blk_el = rows * dv;          // elements of one head inside one pipeline block
-  const bool vec4 = (dv % 4) == 0;
-  int per_cta = (blk_el + nctas - 1) / nctas;
-  if (vec4) per_cta = (per_cta + 3) & ~3;
-  const int lo = min(blk_el, cta * per_cta), hi = min(blk_el, lo + per_cta);
-  __shared__ int ok;
-  // back-pressure: my slice of the successor's inbox may only be overwritten once the successor has
-  // consumed it in the previous epoch (one ACK per CTA slice, independent of the block count K)
-  if (threadIdx.x == 0 && L.succ_inbox && !spin_until_geq<SYS>(L.my_ack + cta, epoch - 1)) {
-    atomicExch(err, 1);
-    printf("zgla all-scan: ack wait timed out (deadlock)\n");
-    __trap();
-  }
-  for (int b = 0; b < K; ++b) {
-    const int fidx = b * nctas + cta;
-    if (threadIdx.x == 0) {
-      bool good = true;
-      if (L.inbox) good = spin_until_geq<SYS>(L.flags + fidx, epoch);
-      ok = good;
-      if (!good) {
-        atomicExch(err, 1);
-        printf("zgla all-scan: flag wait timed out (deadlock), block %d\n", b);
-        __trap();
-      }
-    }
-    __syncthreads();
-    if (!ok) return;
-    if (vec4) {
-      // float4 path: all loads of a batch are issued before any use (latency-bound otherwise)
-      const int lo4 = lo >> 2, n4 = (hi - lo) >> 2, blk4 = blk_el >> 2;
-      const int total = h * n4;
-      for (int u0 = threadIdx.x; u0 < total; u0 += 4 * blockDim.x) {
-        V4<T> r[4], x[4];
-        T gl[4];
-        long long e4[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int u = u0 + k * blockDim.x;
-          const int hh = u / max(n4, 1), i4 = lo4 + u % max(n4, 1);
-          e4[k] = ((long long)hh * dk * dv + (long long)b * blk_el) / 4 + i4;
-          if (u < total) {
-            const int c = b * rows + (i4 * 4) / dv;
-            gl[k] = L.logdecay[hh * dk + c];
-            x[k] = reinterpret_cast<const V4<T>*>(L.local)[e4[k]];
-            r[k] = L.inbox ? ldcg4(reinterpret_cast<const V4<T>*>(L.inbox) + e4[k]) : V4<T>{0, 0, 0, 0};
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (u0 + k * blockDim.x >= total) break;
-          V4<T> sc;
-          sc.x = scan_update(gl[k], r[k].x, x[k].x);
-          sc.y = scan_update(gl[k], r[k].y, x[k].y);
-          sc.z = scan_update(gl[k], r[k].z, x[k].z);
-          sc.w = scan_update(gl[k], r[k].w, x[k].w);
-          if (L.recv_out) reinterpret_cast<V4<T>*>(L.recv_out)[e4[k]] = r[k];
-          reinterpret_cast<V4<T>*>(L.scanned_out)[e4[k]] = sc;
-          if (L.succ_inbox) reinterpret_cast<V4<T>*>(L.succ_inbox)[e4[k]] = sc;
-        }
-      }
-      (void)blk4;
-    } else {
-      for (int hh = 0; hh < h; ++hh) {
-        const long long base = (long long)hh * dk * dv + (long long)b * blk_el;
-        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-          const long long e = base + i;
-          const int c = b * rows + i / dv;
-          const T r = L.inbox ? ldcg(L.inbox + e) : T(0);
-          // same rounding sequence as the reference update (gate * recv, then + local)
-          const T s = scan_update(L.logdecay[hh * dk + c], r, L.local[e]);
-          if (L.recv_out) L.recv_out[e] = r;
-          L.scanned_out[e] = s;
-          if (L.succ_inbox) L.succ_inbox[e] = s;
-        }
-      }
-    }
-    __syncthreads();
-    // release at system scope is cumulative over the CTA's stores observed through bar.sync
-    if (threadIdx.x == 0 && L.succ_inbox) st_release<SYS>(L.succ_flags + fidx, epoch);
-  }
-  if (threadIdx.x == 0 && L.ack_to_pred) st_release<SYS>(L.ack_to_pred + cta, epoch);
-}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// list form: P ranks on one device, recv[p] doubles as rank p's inbox
-template <typename T>
-__global__ void __launch_bounds__(kThreads) local_chain_kernel(int P, int h, int dk, int dv, int K, int dir,
-                                                               const T* local, const T* logdecay, T* recv,
-                                                               T* scanned, unsigned* flags, int* err) {
-  const int pos = blockIdx.x / kCtasPerRank, cta = blockIdx.x % kCtasPerRank;
-  const int rank = dir == ZGLA_FWD ? pos : P - 1 - pos;
-  const long long nel = (long long)h * dk * dv;
-  const int succ = dir == ZGLA_FWD ? rank + 1 : rank - 1;
-  const int fl = K * kCtasPerRank;
-  Link<T> L;
-  L.local = local + rank * nel;
-  L.logdecay = logdecay + (long long)rank * h * dk;
-  L.inbox = pos == 0 ? nullptr : recv + rank * nel;
-  L.flags = flags + (long long)rank * fl;
-  L.ack_to_pred = nullptr;
-  L.succ_inbox = pos == P - 1 ? nullptr : recv + (long long)succ * nel;
-  L.succ_flags = pos == P - 1 ? nullptr : flags + (long long)succ * fl;
-  L.my_ack = nullptr;
-  L.recv_out = pos == 0 ? recv + rank * nel : nullptr;  // source writes its zero recv
-  L.scanned_out = scanned + rank * nel;
-  if (L.succ_inbox) {
-    // no ACK protocol needed: flags are cleared before every list-form call
-    L.my_ack = flags + (long long)P * fl;  // all-zero dummy; epoch-1 == 0 passes
-  }
-  rank_body<T, false>(L, h, dk, dv, K, cta, kCtasPerRank, 1u, err);  // one device: gpu scope
-}
-
-// SPMD form: one rank per process
-// The epoch lives in device memory (ctl[0]) so that a captured CUDA graph replays correctly: every
-// CTA reads the completed-call count at entry (the previous call on this stream has finished), and the
-// last CTA to leave publishes the new count (ctl[1] counts departures).
-__global__ void __launch_bounds__(kThreads) rank_chain_kernel(Link<float> L, int h, int dk, int dv, int K,
-                                                              unsigned* ctl, int* err) {
-  const unsigned epoch = *reinterpret_cast<volatile unsigned*>(ctl) + 1;
-  rank_body<float, true>(L, h, dk, dv, K, blockIdx.x, gridDim.x, epoch, err);  // peers: system scope
+// last CTA to leave publishes the completed-call count (and, in the SPMD form, the ACK to the
+// predecessor: a release at system scope, cumulative over the inbox reads of every CTA observed through
+// the bar.sync / departure-counter chain).  The data path itself needs no fence: LL words carry their flag.
+__device__ __forceinline__ void depart(unsigned* ctl, unsigned epoch, unsigned* pred_ack) {
+  __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(ctl + 1, 1u) == gridDim.x - 1) {
+      __threadfence();
       ctl[1] = 0;
+      if (pred_ack) st_release_sys(pred_ack, epoch);
       *reinterpret_cast<volatile unsigned*>(ctl) = epoch;
     }
   }
 }
 
-// list-form workspace (flags + error word), grown on demand
+// list form: P ranks on one device, one kernel; rank r's inbox is inbox + r * nwords.  The epoch is a
+// call counter kept in device memory; inbox words of earlier calls carry older epochs, so no reset
+// pass is needed between calls.
+template <typename T, int EPW>
+__global__ void __launch_bounds__(kThreads) local_chain_kernel(int P, int h, int dk, int dv, int K, int dir,
+                                                               int nctas, const T* local, const T* logdecay,
+                                                               T* recv, T* scanned, uint4* inbox,
+                                                               long long nwords, unsigned* ctl, int* err,
+                                                               unsigned long long timeout_ns,
+                                                               unsigned long long* trace) {
+  unsigned long long* tr = trace ? trace + 4 * blockIdx.x : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtimer();
+  const unsigned epoch = *reinterpret_cast<volatile unsigned*>(ctl) + 1;
+  const int pos = blockIdx.x / nctas, cta = blockIdx.x % nctas;
+  const int rank = dir == ZGLA_FWD ? pos : P - 1 - pos;
+  const int succ = dir == ZGLA_FWD ? rank + 1 : rank - 1;
+  const long long nel = (long long)h * dk * dv;  // (< 2^31: states are at most a few MiB)
+  Chain<T> A;
+  A.local = local + rank * nel;
+  A.logdecay = logdecay + (long long)rank * h * dk;
+  A.inbox = pos == 0 ? nullptr : inbox + rank * nwords;
+  A.succ_inbox = pos == P - 1 ? nullptr : inbox + (long long)succ * nwords;
+  A.recv_out = recv + rank * nel;
+  A.scanned_out = scanned + rank * nel;
+  const unsigned long long deadline = gtimer() + timeout_ns;
+  if (!chain_slice<T, EPW, kBatchList>(A, (int)(nel / EPW), dv, cta, nctas, epoch, deadline, tr))
+    atomicExch(err, ZGLA_ERR_DEADLOCK);
+  depart(ctl, epoch, nullptr);
+  if (tr && threadIdx.x == 0) tr[3] = gtimer();
+}
+
+// SPMD form: one rank per process.  ctl = {completed calls, departures} of this direction in device
+// memory (a captured CUDA graph replays correctly); my_ack is written by the successor.
+__global__ void __launch_bounds__(kThreads, 8) rank_chain_kernel(Chain<float> A, int h, int dk, int dv, int K,
+                                                                 int epw, const uint4* inbox2, uint4* succ_inbox2,
+                                                                 long long nwords, unsigned* ctl,
+                                                                 const unsigned* my_ack, unsigned* pred_ack,
+                                                                 int* err, unsigned long long timeout_ns) {
+  pdl_wait();  // the local state comes from the kernel before (programmatic launch)
+  pdl_trigger();
+  const unsigned epoch = *reinterpret_cast<volatile unsigned*>(ctl) + 1;
+  const unsigned long long deadline = gtimer() + timeout_ns;
+  const int par = epoch & 1;
+  A.inbox = inbox2 ? inbox2 + par * nwords : nullptr;
+  A.succ_inbox = succ_inbox2 ? succ_inbox2 + par * nwords : nullptr;
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    ok = 1;
+    // the successor must have consumed the buffer of this parity (epoch - 2) before it is overwritten
+    if (A.succ_inbox && epoch > 2) {
+      unsigned spins = 0;
+      while ((int)(ld_acquire_sys(my_ack) - (epoch - 2)) < 0) {
+        if ((++spins & 255u) == 0 && gtimer() > deadline) {
+          ok = 0;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  bool good = ok != 0;
+  if (good) {
+    const int nw = (int)((long long)h * dk * dv / epw);
+    good = epw == 2 ? chain_slice<float, 2, kBatchRank>(A, nw, dv, blockIdx.x, gridDim.x, epoch, deadline)
+                    : chain_slice<float, 1, kBatchRank>(A, nw, dv, blockIdx.x, gridDim.x, epoch, deadline);
+  }
+  if (!good) atomicExch(err, ZGLA_ERR_DEADLOCK);
+  depart(ctl, epoch, pred_ack);
+}
+
+inline int epw_for(int dv, bool f64) { return (f64 || dv % 2) ? 1 : 2; }  // a word never straddles a row
+inline int ctas_for(long long nwords, int cap = kMaxCtas, int wpt = kWordsPerThread / 2) {
+  long long n = (nwords + (long long)kThreads * wpt - 1) / ((long long)kThreads * wpt);
+  return (int)std::max(1ll, std::min((long long)cap, n));
+}
+inline unsigned long long timeout_ns_default() {
+  static const unsigned long long t = [] {
+    const char* e = std::getenv("ZGLA_ALLSCAN_TIMEOUT_MS");
+    const long long ms = e ? std::atoll(e) : 10000;
+    return (unsigned long long)(ms > 0 ? ms : 10000) * 1000000ull;
+  }();
+  return t;
+}
+
+// host-mapped error word: the kernel reports a timed-out wait without trapping, the host reads it
+// without a device synchronisation
+struct MappedErr {
+  int* host = nullptr;
+  int* dev = nullptr;
+  int alloc() {
+    if (host) return ZGLA_OK;
+    if (cudaError_t e = cudaHostAlloc(&host, 64, cudaHostAllocMapped)) return cuda_fail(e, "cudaHostAlloc");
+    std::memset(host, 0, 64);
+    if (cudaError_t e = cudaHostGetDevicePointer(&dev, host, 0)) return cuda_fail(e, "cudaHostGetDevicePointer");
+    return ZGLA_OK;
+  }
+  void release() {
+    if (host) cudaFreeHost(host);
+    host = dev = nullptr;
+  }
+};
+
+// list-form workspace (inboxes + control words), grown on demand
 struct Scratch {
   std::mutex mu;
-  unsigned* flags = nullptr;
+  unsigned char* base = nullptr;
   size_t bytes = 0;
+  MappedErr err;
 };
 static Scratch g_scratch;
 
@@ -261,6 +340,29 @@ static Scratch g_scratch;
 using namespace zgla;
 using namespace zgla::allscan;
 
+template <typename... Exp, typename... Act>
+static cudaError_t launch_ex(bool pdl, void (*kern)(Exp...), int grid, int block, cudaStream_t st, Act&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
+}
+
+static bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("ZGLA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 extern "C" int zgla_allscan_local(int P, int heads, int key_dim, int value_dim, int dtype, int num_blocks,
                                   int direction, const void* local_states, const void* log_decays, void* recv,
                                   void* scanned, void* stream) {
@@ -268,35 +370,58 @@ extern "C" int zgla_allscan_local(int P, int heads, int key_dim, int value_dim, 
   if (num_blocks < 1 || key_dim % num_blocks) return ZGLA_ERR_CONFIG;
   if (direction != ZGLA_FWD && direction != ZGLA_BWD) return ZGLA_ERR_CONFIG;
   if (dtype != ZGLA_F32 && dtype != ZGLA_F64) return ZGLA_ERR_UNSUPPORTED;
+  if (!local_states || !log_decays || !recv || !scanned) return ZGLA_ERR_DIMS;
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t fl = (size_t)num_blocks * kCtasPerRank;
-  const size_t need = ((size_t)(P + 1) * fl + 1) * sizeof(unsigned);
+  const bool f64 = dtype == ZGLA_F64;
+  const int epw = epw_for(value_dim, f64);
+  const long long nel = (long long)heads * key_dim * value_dim;
+  const long long nwords = nel / epw;
+  const int nctas = ctas_for(nwords, std::max(1, kMaxListCtas / P), kWordsPerThread);
+  const size_t need = 256 + (size_t)P * nwords * sizeof(uint4);
   std::lock_guard<std::mutex> lock(g_scratch.mu);
+  if (int rc = g_scratch.err.alloc()) return rc;
+  if (*reinterpret_cast<volatile int*>(g_scratch.err.host)) {
+    g_scratch.err.host[0] = 0;
+    set_error("a previous zgla_allscan_local call timed out waiting for its predecessor");
+    return ZGLA_ERR_DEADLOCK;
+  }
   if (g_scratch.bytes < need) {
-    if (g_scratch.flags) cudaFree(g_scratch.flags);
-    g_scratch.flags = nullptr;
+    if (g_scratch.base) {
+      cudaStreamSynchronize(st);
+      cudaFree(g_scratch.base);
+    }
+    g_scratch.base = nullptr;
     g_scratch.bytes = 0;
-    if (cudaError_t e = cudaMalloc(&g_scratch.flags, need)) return cuda_fail(e, "zgla_allscan_local");
+    if (cudaError_t e = cudaMalloc(&g_scratch.base, need)) return cuda_fail(e, "zgla_allscan_local");
+    // zero flags never match an epoch (>= 1); the call counter starts at 0
+    if (cudaError_t e = cudaMemsetAsync(g_scratch.base, 0, need, st)) return cuda_fail(e, "zgla_allscan_local");
     g_scratch.bytes = need;
   }
-  if (cudaError_t e = cudaMemsetAsync(g_scratch.flags, 0, need, st)) return cuda_fail(e, "zgla_allscan_local");
-  int* err = reinterpret_cast<int*>(g_scratch.flags + (P + 1) * fl);
-  if (dtype == ZGLA_F64)
-    local_chain_kernel<double><<<P * kCtasPerRank, kThreads, 0, st>>>(
-        P, heads, key_dim, value_dim, num_blocks, direction, (const double*)local_states, (const double*)log_decays,
-        (double*)recv, (double*)scanned, g_scratch.flags, err);
+  unsigned* ctl = reinterpret_cast<unsigned*>(g_scratch.base);
+  uint4* inbox = reinterpret_cast<uint4*>(g_scratch.base + 256);
+  const unsigned long long to = timeout_ns_default();
+  cudaError_t e;
+  if (f64)
+    e = launch_ex(false, local_chain_kernel<double, 1>, P * nctas, kThreads, st, P, heads, key_dim, value_dim,
+                  num_blocks, direction, nctas, (const double*)local_states, (const double*)log_decays,
+                  (double*)recv, (double*)scanned, inbox, nwords, ctl, g_scratch.err.dev, to, g_trace_buf);
+  else if (epw == 2)
+    e = launch_ex(false, local_chain_kernel<float, 2>, P * nctas, kThreads, st, P, heads, key_dim, value_dim,
+                  num_blocks, direction, nctas, (const float*)local_states, (const float*)log_decays, (float*)recv,
+                  (float*)scanned, inbox, nwords, ctl, g_scratch.err.dev, to, g_trace_buf);
   else
-    local_chain_kernel<float><<<P * kCtasPerRank, kThreads, 0, st>>>(
-        P, heads, key_dim, value_dim, num_blocks, direction, (const float*)local_states, (const float*)log_decays,
-        (float*)recv, (float*)scanned, g_scratch.flags, err);
+    e = launch_ex(false, local_chain_kernel<float, 1>, P * nctas, kThreads, st, P, heads, key_dim, value_dim,
+                  num_blocks, direction, nctas, (const float*)local_states, (const float*)log_decays, (float*)recv,
+                  (float*)scanned, inbox, nwords, ctl, g_scratch.err.dev, to, g_trace_buf);
+  if (e != cudaSuccess) return cuda_fail(e, "local_chain_kernel");
   return zgla_check_launch();
 }
 
 extern "C" int zgla_release_cached(void) {
   std::lock_guard<std::mutex> lock(g_scratch.mu);
-  if (g_scratch.flags) {
-    cudaError_t e = cudaFree(g_scratch.flags);
-    g_scratch.flags = nullptr;
+  if (g_scratch.base) {
+    cudaError_t e = cudaFree(g_scratch.base);
+    g_scratch.base = nullptr;
     g_scratch.bytes = 0;
     if (e != cudaSuccess) return cuda_fail(e, "zgla_release_cached");
   }
@@ -304,34 +429,30 @@ extern "C" int zgla_release_cached(void) {
 }
 
 // ------------------------------------------------------------------ SPMD comm
+// region layout, per direction d: [inbox parity 0 | inbox parity 1] (nwords uint4 each) then
+// control words {ctl[0] epoch, ctl[1] departures, ack}
 struct zgla_allscan_comm {
   int rank, world, h, dk, dv, max_blocks;
-  long long nel;
+  long long nel, nwords;  // nwords: LL words per inbox buffer (worst case EPW = 1 when dv is odd)
   size_t region_bytes;
-  unsigned char* region;  // [dir][inbox | flags | ack]
+  unsigned char* region;
   unsigned char* next_region;
   unsigned char* prev_region;
   bool next_ipc, prev_ipc;
-  int* err;  // [0] deadlock flag; [2 + 2 d], [3 + 2 d]: per-direction device epoch and departure count
+  MappedErr err;
+  unsigned long long timeout_ns;
   long long bytes_sent;
+  bool broken;
 };
 
-static size_t dir_bytes(const zgla_allscan_comm* c) {
-  const size_t fl = (size_t)c->max_blocks * kCtasPerRank * sizeof(unsigned);
-  size_t inbox = (size_t)c->nel * sizeof(float);
-  inbox = (inbox + 255) & ~size_t(255);
-  return inbox + 2 * fl;
+static size_t dir_bytes(const zgla_allscan_comm* c) { return 2 * (size_t)c->nwords * sizeof(uint4) + 256; }
+static uint4* inbox_of(const zgla_allscan_comm* c, unsigned char* region, int dir) {
+  return reinterpret_cast<uint4*>(region + dir * dir_bytes(c));
 }
-static float* inbox_of(const zgla_allscan_comm* c, unsigned char* region, int dir) {
-  return reinterpret_cast<float*>(region + dir * dir_bytes(c));
+static unsigned* ctl_of(const zgla_allscan_comm* c, unsigned char* region, int dir) {
+  return reinterpret_cast<unsigned*>(region + dir * dir_bytes(c) + 2 * (size_t)c->nwords * sizeof(uint4));
 }
-static unsigned* flags_of(const zgla_allscan_comm* c, unsigned char* region, int dir) {
-  size_t inbox = ((size_t)c->nel * sizeof(float) + 255) & ~size_t(255);
-  return reinterpret_cast<unsigned*>(region + dir * dir_bytes(c) + inbox);
-}
-static unsigned* ack_of(const zgla_allscan_comm* c, unsigned char* region, int dir) {
-  return flags_of(c, region, dir) + (size_t)c->max_blocks * kCtasPerRank;
-}
+static unsigned* ack_of(const zgla_allscan_comm* c, unsigned char* region, int dir) { return ctl_of(c, region, dir) + 2; }
 
 extern "C" int zgla_allscan_create(int rank, int world, int heads, int key_dim, int value_dim, int max_blocks,
                                    zgla_allscan_comm** out) {
@@ -346,21 +467,23 @@ extern "C" int zgla_allscan_create(int rank, int world, int heads, int key_dim, 
   c->dv = value_dim;
   c->max_blocks = max_blocks;
   c->nel = (long long)heads * key_dim * value_dim;
+  c->nwords = value_dim % 2 == 0 ? c->nel / 2 : c->nel;
   c->region_bytes = 2 * dir_bytes(c);
+  c->timeout_ns = timeout_ns_default();
   c->bytes_sent = 0;
+  c->broken = false;
   c->next_region = c->prev_region = nullptr;
   c->next_ipc = c->prev_ipc = false;
   if (cudaError_t e = cudaMalloc(&c->region, c->region_bytes)) {
     delete c;
     return cuda_fail(e, "zgla_allscan_create");
   }
-  cudaMemset(c->region, 0, c->region_bytes);
-  if (cudaError_t e = cudaMalloc(&c->err, 8 * sizeof(int))) {
+  if (int rc = c->err.alloc()) {
     cudaFree(c->region);
     delete c;
-    return cuda_fail(e, "zgla_allscan_create");
+    return rc;
   }
-  cudaMemset(c->err, 0, 8 * sizeof(int));
+  cudaMemset(c->region, 0, c->region_bytes);
   if (cudaError_t e = cudaDeviceSynchronize()) return cuda_fail(e, "zgla_allscan_create");
   *out = c;
   return ZGLA_OK;
@@ -404,11 +527,25 @@ extern "C" int zgla_allscan_bind_local(zgla_allscan_comm* c, zgla_allscan_comm* 
   return ZGLA_OK;
 }
 
+extern "C" int zgla_allscan_status(zgla_allscan_comm* c, int sync) {
+  if (!c) return ZGLA_ERR_DIMS;
+  if (sync) {
+    if (cudaError_t e = cudaDeviceSynchronize()) return cuda_fail(e, "zgla_allscan_status");
+  }
+  if (c->broken || *reinterpret_cast<volatile int*>(c->err.host)) {
+    c->broken = true;
+    set_error("All-Scan: a flag / ack wait timed out (a peer never arrived); the communicator is unusable");
+    return ZGLA_ERR_DEADLOCK;
+  }
+  return ZGLA_OK;
+}
+
 extern "C" int zgla_allscan_run(zgla_allscan_comm* c, int num_blocks, int direction, const float* local_state,
                                 const float* log_decay, float* recv, float* scanned, void* stream) {
   if (!c || !local_state || !log_decay || !scanned) return ZGLA_ERR_DIMS;
-  if (num_blocks < 1 || num_blocks > c->max_blocks || c->dk % num_blocks) return ZGLA_ERR_CONFIG;
+  if (num_blocks < 1 || num_blocks > c->dk || c->dk % num_blocks) return ZGLA_ERR_CONFIG;
   if (direction != ZGLA_FWD && direction != ZGLA_BWD) return ZGLA_ERR_CONFIG;
+  if (int rc = zgla_allscan_status(c, 0)) return rc;  // an earlier call timed out
   cudaStream_t st = (cudaStream_t)stream;
   const int d = direction;
   // chain order: FWD 0 -> P-1, BWD P-1 -> 0
@@ -416,26 +553,31 @@ extern "C" int zgla_allscan_run(zgla_allscan_comm* c, int num_blocks, int direct
   const bool is_sink = d == ZGLA_FWD ? c->rank == c->world - 1 : c->rank == 0;
   unsigned char* succ = d == ZGLA_FWD ? c->next_region : c->prev_region;
   unsigned char* pred = d == ZGLA_FWD ? c->prev_region : c->next_region;
-  if ((!is_sink && !succ) || (!is_source && !pred)) return ZGLA_ERR_STATE;  // not bound
-  Link<float> L;
-  L.local = local_state;
-  L.logdecay = log_decay;
-  L.inbox = is_source ? nullptr : inbox_of(c, c->region, d);
-  L.flags = flags_of(c, c->region, d);
-  L.ack_to_pred = is_source ? nullptr : ack_of(c, pred, d);
-  L.succ_inbox = is_sink ? nullptr : inbox_of(c, succ, d);
-  L.succ_flags = is_sink ? nullptr : flags_of(c, succ, d);
-  L.my_ack = ack_of(c, c->region, d);
-  // recv is written by the chain kernel itself (zeros at the source), before the inbox is acked: a
-  // predecessor running ahead into the next epoch can never overwrite data not yet copied out
-  L.recv_out = recv;
-  L.scanned_out = scanned;
-  if (c->world == 1) L.inbox = nullptr;
-  unsigned* ctl = reinterpret_cast<unsigned*>(c->err) + 2 + 2 * d;
-  rank_chain_kernel<<<kCtasPerRank, kThreads, 0, st>>>(L, c->h, c->dk, c->dv, num_blocks, ctl, c->err);
+  if ((!is_sink && !succ) || (!is_source && !pred)) {
+    set_error("All-Scan communicator is not bound to its chain neighbours");
+    return ZGLA_ERR_STATE;
+  }
+  const int epw = epw_for(c->dv, false);
+  const long long nwords = c->nwords;  // buffer stride; a call uses nel / epw of them
+  Chain<float> A;
+  A.local = local_state;
+  A.logdecay = log_decay;
+  A.inbox = nullptr;
+  A.succ_inbox = nullptr;
+  A.recv_out = recv;
+  A.scanned_out = scanned;
+  const uint4* inbox2 = is_source || c->world == 1 ? nullptr : inbox_of(c, c->region, d);
+  uint4* succ_inbox2 = is_sink ? nullptr : inbox_of(c, succ, d);
+  unsigned* ctl = ctl_of(c, c->region, d);
+  const unsigned* my_ack = ack_of(c, c->region, d);
+  unsigned* pred_ack = is_source ? nullptr : ack_of(c, pred, d);
+  const int nctas = ctas_for(c->nel / epw);
+  if (cudaError_t e = launch_ex(pdl_on(), rank_chain_kernel, nctas, kThreads, st, A, c->h, c->dk, c->dv, num_blocks,
+                                epw, inbox2, succ_inbox2, nwords, ctl, my_ack, pred_ack, c->err.dev, c->timeout_ns))
+    return cuda_fail(e, "rank_chain_kernel");
   if (int rc = zgla_check_launch()) return rc;
   if (!is_sink) c->bytes_sent += c->nel * (long long)sizeof(float);
-  return zgla_check_launch();
+  return ZGLA_OK;
 }
 
 extern "C" int zgla_allscan_info(const zgla_allscan_comm* c, int* rank, int* world, int* heads) {
@@ -450,11 +592,13 @@ extern "C" long long zgla_allscan_bytes_sent(const zgla_allscan_comm* c) { retur
 
 extern "C" int zgla_allscan_destroy(zgla_allscan_comm* c) {
   if (!c) return ZGLA_OK;
+  // callers synchronise all ranks (device sync + barrier) before destroying, so no peer still writes
+  // into this region or reads from a mapping closed here (distributed.AllScanP2P.close)
   cudaDeviceSynchronize();
   if (c->next_ipc && c->next_region) cudaIpcCloseMemHandle(c->next_region);
   if (c->prev_ipc && c->prev_region) cudaIpcCloseMemHandle(c->prev_region);
   cudaFree(c->region);
-  cudaFree(c->err);
+  c->err.release();
   delete c;
   return ZGLA_OK;
 }

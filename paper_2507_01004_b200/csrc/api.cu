@@ -193,14 +193,24 @@ extern "C" int zgla_zeco_bwd_output(const zgla_shape* s, int num_sms, const void
   return zgla_zeco_bwd_output_v(s, num_sms, &tq, &tk, &tv, &tg, &td, ws, s_prev, ds_next, &a, &b, &c, &e, stream);
 }
 
+namespace zgla {
+int watch_domain(const void* ws, int** host_flag);
+int unwatch_domain(const void* ws);
+}
+extern "C" int zgla_zeco_watch_domain(void* ws, int** host_flag) {
+  if (!ws || !host_flag) return ZGLA_ERR_DIMS;
+  return zgla::watch_domain(ws, host_flag);
+}
+extern "C" int zgla_zeco_unwatch_domain(void* ws) { return zgla::unwatch_domain(ws); }
+
 extern "C" int zgla_zeco_domain_check(const zgla_shape* s, int num_sms, const void* ws, void* stream) {
   if (int rc = validate_zeco(s, num_sms)) return rc;
   if (!fast_supported(s)) return ZGLA_OK;  // the SIMT paths use the exact token recurrence: any gate
   int flag = 0;
   if (int rc = fast_domain_flag(s, num_sms, ws, &flag, (cudaStream_t)stream)) return rc;
   if (flag) {
-    set_error("a 64-token tile's log-decay is below -160 (or not finite): outside the fused bf16 path's "
-              "exponent domain; use the fp32 validation mode for such gates");
+    set_error("a log-decay entry is >= 0 or not finite (glasp/gla.py:106-107), or a 64-token tile's summed "
+              "log-decay is below -160 (outside the fused bf16 path's exponent domain: use the fp32 mode)");
     return ZGLA_ERR_DOMAIN;
   }
   return ZGLA_OK;

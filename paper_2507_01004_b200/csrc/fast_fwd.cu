@@ -16,6 +16,8 @@
 //   the tile (in-chunk reference point: |exponent| <= |gamma|/2).
 //   The incoming state of every segment already contains the cross-rank
 //   correction e^{G_t} S_prev (fused, no extra pass over HBM).
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 #include "fast_common.cuh"
 
@@ -33,7 +35,8 @@ template <int DIR, bool DENSE>  // 0: forward local state (a=k, b=v, reverse wal
 __global__ void __launch_bounds__(KS_THREADS, 1)
     seg_state_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                      const __grid_constant__ CUtensorMap tm_g, long long L, int in3d, int nseg, int ntiles,
-                     float* __restrict__ out_state, float* __restrict__ out_gam, int* __restrict__ flags) {
+                     float* __restrict__ out_state, float* __restrict__ out_gam, int* __restrict__ flags,
+                     int* dom_sink) {
   extern __shared__ uint8_t smem_raw[];
   // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -134,10 +137,16 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
       float lb[64];
 #pragma unroll
       for (int r = 0; r < 64; ++r) lb[r] = gs[r * D + c];
+      if (DIR == 0) {  // the reference's SeqShard check (glasp/gla.py:106-107): every gate finite and < 0
+        float mx = lb[0];
+#pragma unroll
+        for (int r = 1; r < 64; ++r) mx = fmaxf(mx, lb[r]);
+        if (!(mx < 0.f)) bad = 1;
+      }
 #pragma unroll
       for (int r = 1; r < 64; ++r) lb[r] += lb[r - 1];
       const float gam = lb[63];
-      if (DIR == 0 && !(gam >= -2.f * DOMAIN_EXP)) bad = 1;  // also catches NaN
+      if (DIR == 0 && !(gam >= -2.f * DOMAIN_EXP)) bad = 1;  // also catches NaN / -inf
       xg[(i & 3) * D + c] = gam;
       mbar_arrive(&gready[i & 3]);
       if (i >= 1) {  // gamma of tile i-1 (other group)
@@ -182,6 +191,8 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
   // one domain flag word per CTA, written every call: no reset pass is needed before the kernel
   bad = __syncthreads_or(bad);
   if (DIR == 0 && flags != nullptr && threadIdx.x == 0) flags[blockIdx.x] = bad;
+  // lazy host-visible report (zgla_zeco_watch_domain): host-mapped word, written only when a tile is bad
+  if (DIR == 0 && dom_sink != nullptr && threadIdx.x == 0 && bad) *reinterpret_cast<volatile int*>(dom_sink) = 1;
   if (warp == 9) tmem_dealloc(tbase, 128);
 }
 
@@ -701,9 +712,10 @@ bool fast_supported(const zgla_shape* s) {
 }
 
 long long fast_ws_bytes(const zgla_shape* s, int num_sms) { return ws_bytes(make_plan(s, num_sms)); }
+int* domain_sink_of(const void* ws);
 
 int launch_seg_state(int dir, const Plan& pl, const TRef& a, const TRef& b, const TRef& g, float* out_state,
-                     float* out_gam, int* flags, cudaStream_t st) {
+                     float* out_gam, int* flags, cudaStream_t st, int* dom_sink = nullptr) {
   CUtensorMap ma, mb, mg;
   const bool dn = is_dense(a, pl.L) && is_dense(b, pl.L) && is_dense(g, pl.L);  // all TMA-read
   if (int rc = map_act(&ma, a, pl.L, pl.h, dn)) return rc;
@@ -712,7 +724,7 @@ int launch_seg_state(int dir, const Plan& pl, const TRef& a, const TRef& b, cons
   auto kern = dir == 0 ? seg_state_kernel<0, true> : seg_state_kernel<1, true>;
   set_smem_once((const void*)kern, (int)KS_SMEM);
   if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, KS_THREADS, KS_SMEM, st, ma, mb, mg, pl.L, dn ? 0 : 1, pl.nseg,
-                                pl.ntiles, out_state, out_gam, flags))
+                                pl.ntiles, out_state, out_gam, flags, dom_sink))
     return cuda_fail(e, "seg_state_kernel");
   return zgla_check_launch();
 }
@@ -721,7 +733,7 @@ int fast_fwd_local(const zgla_shape* s, int num_sms, const TRef& k, const TRef& 
                    void* s_local, void* g_tot, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
-  if (int rc = launch_seg_state(0, pl, k, v, g, w.dS, w.gam, w.flags, st)) return rc;
+  if (int rc = launch_seg_state(0, pl, k, v, g, w.dS, w.gam, w.flags, st, domain_sink_of(ws))) return rc;
   const long long n = (long long)pl.h * D * D;
   if (cudaError_t e = launch_k(seg_scan_kernel<0>, (unsigned)((n / 4 + 127) / 128), 128, 0, st, pl.h, pl.nseg, k.dr,
                                 (const float*)w.dS, (const float*)w.gam, w.Sin, w.cumG, (float*)s_local, (float*)g_tot,
@@ -774,6 +786,40 @@ int fast_bwd_local(const zgla_shape* s, int num_sms, const TRef& q, const TRef& 
 }  // namespace zgla
 
 namespace zgla {
+// ---- lazy domain reports: workspace -> host-mapped flag word (zgla_zeco_watch_domain)
+namespace {
+std::mutex g_dom_mu;
+std::unordered_map<const void*, std::pair<int*, int*>> g_dom;  // ws -> (host, device) pointers
+}  // namespace
+int* domain_sink_of(const void* ws) {
+  std::lock_guard<std::mutex> lock(g_dom_mu);
+  auto it = g_dom.find(ws);
+  return it == g_dom.end() ? nullptr : it->second.second;
+}
+int watch_domain(const void* ws, int** host_flag) {
+  std::lock_guard<std::mutex> lock(g_dom_mu);
+  auto it = g_dom.find(ws);
+  if (it == g_dom.end()) {
+    int* h = nullptr;
+    int* d = nullptr;
+    if (cudaError_t e = cudaHostAlloc(&h, sizeof(int), cudaHostAllocMapped)) return cuda_fail(e, "cudaHostAlloc");
+    *h = 0;
+    if (cudaError_t e = cudaHostGetDevicePointer(&d, h, 0)) return cuda_fail(e, "cudaHostGetDevicePointer");
+    it = g_dom.emplace(ws, std::make_pair(h, d)).first;
+  }
+  if (host_flag) *host_flag = it->second.first;
+  return ZGLA_OK;
+}
+int unwatch_domain(const void* ws) {
+  std::lock_guard<std::mutex> lock(g_dom_mu);
+  auto it = g_dom.find(ws);
+  if (it != g_dom.end()) {
+    cudaFreeHost(it->second.first);
+    g_dom.erase(it);
+  }
+  return ZGLA_OK;
+}
+
 int fast_domain_flag(const zgla_shape* s, int num_sms, const void* ws, int* host_flag, cudaStream_t st) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, const_cast<void*>(ws));

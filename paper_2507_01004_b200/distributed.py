@@ -23,7 +23,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native, ops
-from .errors import ConfigError
+from .errors import ConfigError, DimsError, UnsupportedError
 
 
 class AllScanP2P:
@@ -50,24 +50,46 @@ class AllScanP2P:
             dist.barrier(group=group)
 
     def __call__(self, local: torch.Tensor, log_decay: torch.Tensor, num_blocks: int = 1, direction: int = 0):
-        """-> (recv, scanned) for this rank; fp32 [h, dk, dv] / [h, dk]."""
-        recv = torch.empty_like(local)
-        scanned = torch.empty_like(local)
-        _native.call("zgla_allscan_run", self._h, num_blocks, direction, ops._p(local.contiguous()),
-                     ops._p(log_decay.contiguous()), ops._p(recv), ops._p(scanned), ops._stream())
+        """-> (recv, scanned) for this rank; fp32 [h, dk, dv] / [h, dk] CUDA tensors."""
+        h, dk, dv = self.shape
+        for t, name, shp in ((local, "local", (h, dk, dv)), (log_decay, "log_decay", (h, dk))):
+            if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
+                raise UnsupportedError(f"AllScanP2P moves fp32 states: {name} must be a float32 CUDA tensor"
+                                       f" (got {getattr(t, 'dtype', type(t))}); fp64 runs use the list form")
+            if tuple(t.shape) != shp:
+                raise DimsError(f"{name} has shape {tuple(t.shape)}, expected {shp}")
+        # keep the dense copies alive until the (stream-ordered) launch has been enqueued
+        loc = local.contiguous()
+        dec = log_decay.contiguous()
+        recv = torch.empty_like(loc)
+        scanned = torch.empty_like(loc)
+        _native.call("zgla_allscan_run", self._h, num_blocks, direction, ops._p(loc), ops._p(dec), ops._p(recv),
+                     ops._p(scanned), ops._stream())
         return recv, scanned
+
+    def check(self, sync: bool = True) -> None:
+        """DeadlockError if a chain wait of an earlier call timed out (a peer never arrived)."""
+        _native.call("zgla_allscan_status", self._h, 1 if sync else 0)
 
     def bytes_sent(self) -> int:
         return int(_native.load().zgla_allscan_bytes_sent(self._h))
 
     def close(self):
+        """Free the peer-mapped buffers.  Collective when world > 1: every rank drains its device and
+        meets the others in a barrier first, so no peer still stores into (or acks to) this region."""
         if getattr(self, "_h", None):
+            if self.world > 1 and dist.is_initialized():
+                torch.cuda.synchronize()
+                dist.barrier(group=self.group)
             _native.load().zgla_allscan_destroy(self._h)
             self._h = None
 
     def __del__(self):
+        # no collective from a finalizer: only a communicator nobody can still be talking to is freed here
         try:
-            self.close()
+            if getattr(self, "_h", None) and (self.world == 1 or not dist.is_initialized()):
+                _native.load().zgla_allscan_destroy(self._h)
+                self._h = None
         except Exception:
             pass
 
@@ -132,6 +154,7 @@ class ZecoRank:
             raise ConfigError(f"num_blocks {num_blocks} does not divide key dim {dim}")
 
     def forward(self, q, k, v, g, out=None):
+        self.shard.poll_domain()  # lazy: reports a bad gate seen by an earlier, completed call
         s_loc, g_tot = self.shard.fwd_local(k, v, g)
         prev = None
         if self.world > 1:
@@ -188,6 +211,7 @@ class ZecoRank:
         _native.call("zgla_zeco_host_wait", ops._stream())
 
     def backward(self, q, k, v, g, d_out, grads=None):
+        self.shard.poll_domain()
         ds0 = self.shard.bwd_local(q, g, d_out)
         ds_next = None
         if self.world > 1:

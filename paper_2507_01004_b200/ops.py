@@ -254,6 +254,29 @@ class ZecoShard:
             raise DimsError("invalid ZeCO shard geometry")
         self.ws = _ws(nbytes, self.device)
         self.fast = bool(_native.load().zgla_fast_path(ctypes.byref(self.shape)))
+        self._dom = None
+        if self.fast:  # lazy domain reports of the fused forward segment pass (host-mapped word)
+            dom = ctypes.POINTER(ctypes.c_int)()
+            _native.call("zgla_zeco_watch_domain", _p(self.ws), ctypes.byref(dom))
+            self._dom = dom
+
+    def __del__(self):
+        try:
+            if getattr(self, "_dom", None) is not None:
+                _native.load().zgla_zeco_unwatch_domain(_p(self.ws))
+                self._dom = None
+        except Exception:
+            pass
+
+    def poll_domain(self):
+        """Lazy, non-synchronising domain check of the fused path: DomainError if any fwd_local that has
+        COMPLETED since the last poll saw a 64-token tile whose log-decay leaves the bf16 exponent domain
+        (a host-mapped word the segment pass writes only in that case).  ZecoRank polls at every call, so
+        a bad gate surfaces one call late instead of costing a synchronisation per step."""
+        if self._dom is not None and self._dom[0]:
+            self._dom[0] = 0
+            raise DomainError("a log-decay entry is >= 0 or not finite, or a 64-token tile's summed log-decay "
+                              "is below -160 (outside the fused bf16 path's exponent domain: use the fp32 mode)")
 
     def _state(self):
         return torch.empty((self.geo.h, self.geo.dk, self.geo.dv), dtype=self.geo.acc, device=self.device)

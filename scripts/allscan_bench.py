@@ -46,18 +46,51 @@ def timeit(fn, iters=50, warmup=5):
     return statistics.mean(ts), statistics.median(ts)
 
 
+def graph_time(fn, reps=20, iters=10):
+    """per-call device time: `reps` calls captured in one CUDA graph, replayed `iters` times (no host
+    launch overhead inside the timed region); returns (mean, best) in us"""
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3 / reps)
+    return statistics.mean(ts), min(ts)
+
+
 def virtual(P, iters):
-    """All P ranks in ONE launch of the list-form kernel (same rank_body device code as the SPMD
-    kernel, flags/data through device memory + L2): the kernel time is the chain latency."""
-    from paper_2507_01004_b200 import ops
+    """All P ranks in ONE launch of the list-form kernel (same chain_slice device code as the SPMD
+    kernel, LL words through device memory + L2): the kernel time is the chain latency."""
+    from paper_2507_01004_b200 import _native, ops
+    lib = _native.load()
     out = []
     for h, d in SIZES:
         local = torch.rand(P, h, d, d, device="cuda")
         logs = -torch.rand(P, h, d, device="cuda")
+        recv, scanned = torch.empty_like(local), torch.empty_like(local)
         for K in [k for k in BLOCKS if k <= d]:
-            mean, p50 = timeit(lambda: ops.allscan_local(local, logs, K, 0), iters)
-            out.append({"mode": "virtual-ranks-one-gpu (list-form kernel)", "P": P, "H": h, "d": d, "K": K,
-                        "state_bytes": h * d * d * 4, "allscan_us_mean": mean, "allscan_us_p50": p50})
+            def fn():
+                _native.check(lib.zgla_allscan_local(P, h, d, d, _native.ZGLA_F32, K, 0, ops._p(local), ops._p(logs),
+                                                     ops._p(recv), ops._p(scanned), ops._stream()), "allscan")
+            mean, best = graph_time(fn, iters=iters)
+            out.append({"mode": "virtual-ranks-one-gpu (list-form kernel, graph-timed)", "P": P, "H": h, "d": d,
+                        "K": K, "state_bytes": h * d * d * 4, "allscan_us_mean": mean, "allscan_us_best": best,
+                        "tau_min_nvlink_us": h * d * d * 4 / 900e3})
     return out
 
 

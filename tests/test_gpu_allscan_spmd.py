@@ -95,3 +95,53 @@ def test_spmd_matches_list_form_bitwise():
     finally:
         for c in comms:
             lib.zgla_allscan_destroy(c)
+
+
+_DEADLOCK_SCRIPT = r"""
+import ctypes, sys, time
+sys.path.insert(0, sys.argv[1])
+import torch
+from paper_2507_01004_b200 import _native, errors
+from tests.test_gpu_allscan_spmd import make_comms
+lib, comms = make_comms(2, 2, 64, 32)
+local = torch.rand(2, 2, 64, 32, device="cuda")
+logs = -torch.rand(2, 2, 64, device="cuda")
+recv, scanned = torch.empty_like(local), torch.empty_like(local)
+t0 = time.time()
+# only rank 1 runs: its predecessor never stores, so the chain wait must time out (no trap, no hang)
+_native.check(lib.zgla_allscan_run(comms[1], 4, 0, ctypes.c_void_p(local[1].data_ptr()),
+                                   ctypes.c_void_p(logs[1].data_ptr()), ctypes.c_void_p(recv[1].data_ptr()),
+                                   ctypes.c_void_p(scanned[1].data_ptr()), None), "run")
+try:
+    _native.check(lib.zgla_allscan_status(comms[1], 1), "status")
+    print("NO-ERROR")
+except errors.DeadlockError as e:
+    print("DEADLOCK", round(time.time() - t0, 2))
+# the CUDA context is still usable after the timed-out kernel
+x = torch.ones(4, device="cuda") * 3
+print("CTX-OK", float(x.sum()))
+try:  # and the communicator refuses further calls
+    _native.check(lib.zgla_allscan_run(comms[1], 4, 0, ctypes.c_void_p(local[1].data_ptr()),
+                                       ctypes.c_void_p(logs[1].data_ptr()), ctypes.c_void_p(recv[1].data_ptr()),
+                                       ctypes.c_void_p(scanned[1].data_ptr()), None), "run")
+    print("RERUN-ACCEPTED")
+except errors.DeadlockError:
+    print("RERUN-REFUSED")
+"""
+
+
+def test_spmd_timeout_raises_deadlock_not_trap(tmp_path):
+    """A chain wait that never completes reports ZGLA_ERR_DEADLOCK -> DeadlockError (SURVEY §5:
+    bounded-spin timeout -> error code, not a hang) and leaves the CUDA context usable."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "dl.py"
+    script.write_text(_DEADLOCK_SCRIPT)
+    env = dict(os.environ, ZGLA_ALLSCAN_TIMEOUT_MS="300", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, str(script), root], capture_output=True, text=True, timeout=240, env=env,
+                         cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "DEADLOCK" in out.stdout, out.stdout
+    assert "CTX-OK 12.0" in out.stdout and "RERUN-REFUSED" in out.stdout, out.stdout
