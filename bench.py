@@ -149,60 +149,149 @@ def load_traffic():
         return None
 
 
-# ------------------------------------------------------------------ CPU legs (oracle port)
+# ------------------------------------------------------------------ CPU legs (the reference's own CPU path)
 
-def _cpu_heads(args):
-    """worker: f64 oracle ZeCO fwd+bwd on a subset of heads (single-threaded numpy)."""
-    heads, L, D, C, seed = args
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _reference_kind():
+    """'reference' when the unmodified glasp is installed in baseline/_ref (build() does it), else 'port'."""
+    return "reference" if os.path.isfile(os.path.join(REF_DIR, "glasp", "engine.py")) else "port"
+
+
+def _cpu_heads(job):
+    """Worker: one fwd+bwd of the reference CPU path on a subset of heads; returns seconds of compute.
+
+    kind 'reference' runs the unmodified glasp (baseline/_ref) through its public API --
+    run_forward/run_backward(SINGLE_DEVICE) (glasp/engine.py:176-210, 301-345) on
+    generate_sequence inputs (glasp/instances.py:25-51); kind 'port' runs oracle/gla_oracle.py."""
+    heads, L, D, C, seed, kind, P, K = job
+    rng = np.random.default_rng(seed + 1)
+    do = rng.uniform(-1, 1, (heads, P * L, D))
+    if kind == "reference":
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        from glasp.cluster import NetConfig, create_cluster
+        from glasp.collectives import PipelineConfig
+        from glasp.engine import StrategyKind, run_backward, run_forward
+        from glasp.gla import ModelDims
+        from glasp.instances import generate_sequence
+        seq = generate_sequence(P, L, C, ModelDims(heads, D, D), seed)
+        strat = StrategyKind.ZECO if P > 1 else StrategyKind.SINGLE_DEVICE
+        pipe = PipelineConfig(K) if P > 1 else PipelineConfig()
+        t0 = time.perf_counter()
+        art = run_forward(seq, strat, create_cluster(P, NetConfig()), pipe)
+        run_backward(seq, do, strat, create_cluster(P, NetConfig()), pipe, art)
+        return time.perf_counter() - t0
     from oracle import gla_oracle as orc
-    rng = np.random.default_rng(seed)
-    q, k, v = (rng.uniform(-1, 1, (heads, L, D)) for _ in range(3))
-    g = rng.uniform(orc.DECAY_LOW, orc.DECAY_HIGH, (heads, L, D))
-    do = rng.uniform(-1, 1, (heads, L, D))
+    q, k, v, g = orc.make_inputs(P, L, heads, D, D, seed=seed)
     t0 = time.perf_counter()
-    o, saved, _ = orc.zeco_forward(q, k, v, g, 1, C)
-    orc.zeco_backward(q, k, v, g, do, 1, C, saved)
+    o, saved, _ = orc.zeco_forward(q, k, v, g, P, C)
+    orc.zeco_backward(q, k, v, g, do, P, C, saved)
     return time.perf_counter() - t0
 
 
-def cpu_sample(H, L_sample, D, C, workers, seed=0):
-    """Time the oracle on all H heads of an L_sample-token shard, heads spread over `workers` processes."""
-    import multiprocessing as mp
-    per = [H // workers + (1 if i < H % workers else 0) for i in range(workers)]
-    jobs = [(n, L_sample, D, C, seed + i) for i, n in enumerate(per) if n > 0]
-    t0 = time.perf_counter()
-    if len(jobs) == 1:
-        _cpu_heads(jobs[0])
-    else:
-        ctx = mp.get_context("spawn")
-        with ctx.Pool(len(jobs)) as pool:
-            pool.map(_cpu_heads, jobs)
-    return time.perf_counter() - t0
+class CpuPool:
+    """A warm process pool over heads (heads are independent).  Workers are spawned, import the
+    reference and run one untimed map BEFORE any timed region, so timings cover compute only."""
+
+    def __init__(self, H, D, C, kind, workers):
+        import multiprocessing as mp
+        self.H, self.D, self.C, self.kind = H, D, C, kind
+        self.workers = max(1, min(workers, H))
+        saved = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+        for k in saved:  # one BLAS thread per worker: the pool supplies the parallelism
+            os.environ[k] = "1"
+        try:
+            self.pool = mp.get_context("spawn").Pool(self.workers) if self.workers > 1 else None
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        self.run(64)  # warm: imports + first-touch, untimed
+
+    def jobs(self, L, seed=0):
+        per = [self.H // self.workers + (1 if i < self.H % self.workers else 0) for i in range(self.workers)]
+        return [(n, L, self.D, self.C, seed + i, self.kind, 1, 1) for i, n in enumerate(per) if n > 0]
+
+    def run(self, L, seed=0):
+        """Wall seconds for one fwd+bwd of all H heads over an L-token shard."""
+        jobs = self.jobs(L, seed)
+        t0 = time.perf_counter()
+        if self.pool is None:
+            for j in jobs:
+                _cpu_heads(j)
+        else:
+            self.pool.map(_cpu_heads, jobs)
+        return time.perf_counter() - t0
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
+
+
+def cpu_legs(H, D, C, L_sample, repeats, steps_note):
+    """The CPU baseline: the reference path, pool-parallel over heads (headline) + single-process variants."""
+    kind = _reference_kind()
+    cores = os.cpu_count() or 1
+    pool = CpuPool(H, D, C, kind, cores)
+    times = [pool.run(L_sample, seed=s) for s in range(repeats)]
+    pool.close()
+    t = statistics.mean(times)
+    src = ("unmodified glasp 0.1.0 (baseline/_ref) run_forward/run_backward(SINGLE_DEVICE), f64"
+           if kind == "reference" else "oracle/gla_oracle.py (NumPy restatement of glasp), f64")
+    out = {"value": L_sample / t, "unit": UNIT, "cores": pool.workers, "kind": kind,
+           "sample": f"all {H} heads x {L_sample} tokens, d={D}, C={C}, one fwd+bwd per {steps_note}; {src}; "
+                     f"heads spread over {pool.workers} warm spawned processes (1 BLAS thread each), "
+                     f"pool start-up outside the timed region; {cores} host cores",
+           "ms_per_step": t * 1e3}
+    return out
+
+
+def cpu_single_process(H, D, C, L, P, K, seed=0):
+    """Variant: the reference path in THIS process (numpy's own threading), as BASELINE.md section 4 times it."""
+    kind = _reference_kind()
+    dt = _cpu_heads((H, L, D, C, seed, kind, P, K))
+    return {"value": P * L / dt, "unit": UNIT, "seconds": dt, "kind": kind, "processes": 1,
+            "sample": f"H={H}, d={D}, C={C}, {P} rank(s) x {L} tokens, "
+                      f"{'ZECO K=' + str(K) if P > 1 else 'SINGLE_DEVICE'}, f64, one process"}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU algorithm (oracle port, f64 NumPy) on this box's cores."""
+    """--impl reference: the reference's own CPU implementation of the path on this box's host cores."""
     if rank != 0:
         return
+    H, D, C = args.heads, args.dim, args.chunk
+    L_sample = 1024
+    kind = _reference_kind()
     cores = os.cpu_count() or 1
-    workers = max(1, min(cores, args.heads))
-    L_sample = 512
-    for _ in range(max(args.warmup, 0)):
-        cpu_sample(args.heads, L_sample, args.dim, args.chunk, workers)
-    times = [cpu_sample(args.heads, L_sample, args.dim, args.chunk, workers) for _ in range(args.steps)]
-    t = sum(times) / len(times)
-    rate = L_sample / t  # tokens/s of one rank's shard (all heads)
-    sample = f"all {args.heads} heads x {L_sample} tokens, d={args.dim}, C={args.chunk}, f64, per step"
+    pool = CpuPool(H, D, C, kind, cores)
+    for i in range(max(args.warmup, 0)):
+        pool.run(L_sample, seed=1000 + i)
+    times = [pool.run(L_sample, seed=s) for s in range(args.steps)]
+    pool.close()
+    t = statistics.mean(times)
+    rate = L_sample / t
+    src = ("unmodified glasp 0.1.0 (baseline/_ref) run_forward/run_backward(SINGLE_DEVICE), f64"
+           if kind == "reference" else "oracle/gla_oracle.py (NumPy restatement of glasp), f64")
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": "GLA layer fwd+bwd (cfg2: H=16, d=128, 16K tok/GPU), CPU sample", "heads": args.heads,
-                   "head_dim": args.dim, "chunk": args.chunk, "tokens_per_gpu": args.seq},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": sample + "; oracle/gla_oracle.py (NumPy restatement of glasp, f64)"},
+        "dtype": "f64", "data": "synthetic (glasp generate_sequence, seeded)", "impl": "reference",
+        "config": {"workload": "cfg2: GLA layer fwd+bwd, H=16, d_k=d_v=128, 16384 tokens/GPU, chunk 64 "
+                               f"(CPU: bounded sample of {L_sample} tokens x all heads per step)",
+                   "heads": H, "head_dim": D, "chunk": C, "tokens_per_gpu": args.seq},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": pool.workers, "kind": kind,
+                         "sample": f"all {H} heads x {L_sample} tokens per step; {src}; heads over "
+                                   f"{pool.workers} warm processes (pool start-up untimed); {cores} host cores"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "variants": {
+            "single_process_cfg2_sample": cpu_single_process(H, D, C, 256, 1, 1),
+            "single_process_cfg1": cpu_single_process(4, 64, 64, 2048, 2, 4),
+        },
     }
     print(json.dumps(line), flush=True)
 
@@ -417,13 +506,7 @@ def main():
         line["allscan_us"] = {"fwd": per_phase["fwd_allscan"] * 1e3, "bwd": per_phase["bwd_allscan"] * 1e3}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = os.cpu_count() or 1
-        workers = max(1, min(cores, H))
-        L_sample = 512
-        t_cpu = cpu_sample(H, L_sample, D, C, workers)
-        line["cpu_baseline"] = {"value": L_sample / t_cpu, "unit": UNIT, "cores": workers, "kind": "port",
-                                "sample": f"oracle/gla_oracle.py f64 ZeCO fwd+bwd, all {H} heads x {L_sample} "
-                                          f"tokens, d={D}, {workers} processes"}
+        line["cpu_baseline"] = cpu_legs(H, D, C, 1024, 3, "repeat (3 repeats)")
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
