@@ -92,6 +92,17 @@ int zgla_revcum(const zgla_shape* s, int d, const void* x, void* out, void* stre
 /* glasp/gla.py:233 chunk_scalings of one chunk g [h][C][dk] */
 int zgla_chunk_scalings(const zgla_shape* s, const void* g_chunk, void* chunk_decay, void* from_start,
                         void* to_end, void* stream);
+/* glasp/gla.py:210-230 recurrent_forward: the token-by-token recurrence (independent of every chunkwise
+ * kernel).  init may be NULL (zero state); bounds [N+1][h][dk][dv] and final [h][dk][dv] may be NULL. */
+int zgla_recurrent_forward(const zgla_shape* s, const void* q, const void* k, const void* v, const void* g,
+                           const void* init, void* o, void* bounds, void* final_state, void* stream);
+/* glasp/gla.py:447-480 finite_diff_grad, float64 only: losses[i] = sum(probe * recurrent_forward(x_i)) for
+ * perturbations i = first .. first+count-1 of tensor `which` (0 q, 1 k, 2 v, 3 g); perturbation i bumps flat
+ * element i/2 by +step (i even) or -step (i odd).  ZGLA_ERR_UNSUPPORTED if h*dk*dv > zgla_fd_max_state(). */
+long long zgla_fd_max_state(void);
+int zgla_fd_losses(const zgla_shape* s, const double* q, const double* k, const double* v, const double* g,
+                   const double* probe, int which, long long first, long long count, double step, double* losses,
+                   void* stream);
 /* elementwise domain checks used by SeqShard/State validation; *bad set to 1 if violated */
 int zgla_check_log_decay(long long n, int dtype, const void* g, int* bad_dev, void* stream);
 

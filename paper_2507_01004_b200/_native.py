@@ -65,6 +65,9 @@ _SIGS = {
     "zgla_revcum": ([ctypes.POINTER(Shape), _I, _P, _P, _P], _I),
     "zgla_chunk_scalings": ([ctypes.POINTER(Shape), _P, _P, _P, _P, _P], _I),
     "zgla_check_log_decay": ([_LL, _I, _P, _P, _P], _I),
+    "zgla_recurrent_forward": ([ctypes.POINTER(Shape)] + [_P] * 9, _I),
+    "zgla_fd_max_state": ([], _LL),
+    "zgla_fd_losses": ([ctypes.POINTER(Shape), _P, _P, _P, _P, _P, _I, _LL, _LL, ctypes.c_double, _P, _P], _I),
     "zgla_zeco_workspace_bytes": ([ctypes.POINTER(Shape), _I], _LL),
     "zgla_zeco_fwd_local": ([ctypes.POINTER(Shape), _I, _P, _P, _P, _P, _P, _P, _P], _I),
     "zgla_zeco_fwd_output": ([ctypes.POINTER(Shape), _I, _P, _P, _P, _P, _P, _P, _P, _P], _I),

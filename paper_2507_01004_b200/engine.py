@@ -21,9 +21,9 @@ import torch
 
 from . import ops
 from ._convert import acc_of, back, compute_dtype, to_dev
-from .cluster import DeviceCluster, NetConfig, VirtualTimeline, VolumeLedger, create_cluster
+from .cluster import NetConfig, Payload, VirtualCluster, VirtualTimeline, VolumeLedger, create_cluster
 from .collectives import PipelineConfig, ScanDirection, all_scan_device
-from .errors import ConfigError, LayoutError, StateError
+from .errors import ConfigError, DimsError, LayoutError, StateError
 from .gla import CumDecay, GradShard, ModelDims, SeqShard, ShardLayout, State
 
 
@@ -97,17 +97,18 @@ class SavedForward:
     final_states: list
     total_log_decays: list
     local_states: list | None = None
-    # device-side context: per-rank ZecoShard workspaces + device copies of the inputs
-    _ctx: dict | None = field(default=None, repr=False)
 
 
 class RunArtifacts:
-    """Outputs, ledger, measured timeline, boundary states (lazy), grads (glasp/engine.py:130-137)."""
+    """Outputs, ledger, (virtual) timeline, boundary states (lazy), grads (glasp/engine.py:130-137);
+    ``measured_timeline`` adds the CUDA-event intervals of the device phases."""
 
-    def __init__(self, outputs, ledger, timeline, boundary_states=None, grads=None, saved=None, _bounds_fn=None):
+    def __init__(self, outputs, ledger, timeline, boundary_states=None, grads=None, saved=None, _bounds_fn=None,
+                 measured_timeline=None):
         self.outputs = outputs
         self.ledger = ledger
         self.timeline = timeline
+        self.measured_timeline = measured_timeline
         self._boundary = boundary_states
         self._bounds_fn = _bounds_fn
         self.grads = grads
@@ -134,11 +135,24 @@ def _check_cluster(seq, strategy, cluster):
     return cluster
 
 
+def _validate_sequence(seq):
+    """What the reference checks when split() builds each rank's SeqShard (glasp/gla.py:95-107): tensor
+    shapes, and log-decays finite and strictly negative (on the device, one pass)."""
+    h, ek, ev = seq.dims.heads, seq.dims.key_dim, seq.dims.value_dim
+    T = seq.total_len
+    for name, arr, shape in (("q", seq.q, (h, T, ek)), ("k", seq.k, (h, T, ek)), ("v", seq.v, (h, T, ev)),
+                             ("g", seq.g, (h, T, ek))):
+        if tuple(arr.shape) != shape:
+            raise DimsError(f"{name} has shape {tuple(arr.shape)}, expected {shape}")
+
+
 def _device_inputs(seq, P):
-    """Contiguous per-rank device copies (q, k, v, g) in the compute dtype."""
+    """Contiguous per-rank device copies (q, k, v, g) in the compute dtype, read from ``seq`` now."""
+    _validate_sequence(seq)
     dt = compute_dtype(seq.q)
     acc = acc_of(dt)
     full = [to_dev(seq.q, dt), to_dev(seq.k, dt), to_dev(seq.v, dt), to_dev(seq.g, acc)]
+    ops.check_log_decay(full[3])
     T = full[0].shape[1]
     L = T // P
     if P == 1:
@@ -165,13 +179,19 @@ def _boundary_fn(ranks, C, prevs, npo):
     return build
 
 
-def run_forward(seq: GlobalSequence, strategy: StrategyKind, cluster: DeviceCluster | None,
+def run_forward(seq: GlobalSequence, strategy: StrategyKind, cluster: VirtualCluster | None,
                 pipe: PipelineConfig = PipelineConfig(), costs: ComputeCosts = DEFAULT_COSTS,
                 save_all: bool = False) -> RunArtifacts:
-    """Distributed forward pass; outputs cover the full sequence (glasp/engine.py:176-298)."""
+    """Distributed forward pass; outputs cover the full sequence (glasp/engine.py:176-298).
+
+    Device work per rank goes through the ZeCO entry points; the cluster is charged the reference's
+    virtual time for every phase (same labels, streams and durations), so ledger and timeline equal the
+    reference's, while ``RunArtifacts.measured_timeline`` carries the CUDA-event times of the phases."""
     cluster = _check_cluster(seq, strategy, cluster)
     P = 1 if strategy is StrategyKind.SINGLE_DEVICE else seq.num_ranks
     C = seq.layout.chunk_len
+    c = costs.per_chunk
+    N = seq.layout.num_chunks * (seq.num_ranks if strategy is StrategyKind.SINGLE_DEVICE else 1)
     npo = _is_numpy(seq)
     ranks, dt = _device_inputs(seq, P)
     acc = acc_of(dt)
@@ -187,24 +207,35 @@ def run_forward(seq: GlobalSequence, strategy: StrategyKind, cluster: DeviceClus
             with cluster.phase(r, "local_scan"):
                 q, k, v, g = ranks[r]
                 loc.append(shards[r].fwd_local(k, v, g))
+            cluster.compute(r, N * c, "local_scan")
         for sh in shards:  # the fused bf16 path's exponent domain (DomainError, like invalid gates)
             if sh.fast:
                 sh.check_domain()
         finals = torch.stack([x[0] for x in loc])
         totals = torch.stack([x[1] for x in loc])
+        entry = list(cluster.clocks)
         if strategy is StrategyKind.LASP2 and P > 1:
             from .collectives import all_gather_grouped
             all_gather_grouped(cluster, {"all_gather": list(finals), "all_gather_cumdecay": list(totals)})
             # every rank's decay-weighted reduction of the gathered states (glasp/engine.py:165-173)
             with cluster.phase(0, "state_reduce"):
                 prevs_t, scanned_t = ops.allscan_local(finals, totals, 1, 0)
-        else:
+        elif strategy is StrategyKind.ZECO:
             prevs_t, scanned_t = all_scan_device(cluster, finals, totals, pipe, ScanDirection.FWD)
+            for r in range(P):  # the intra-chunk precompute overlaps the collective (glasp/engine.py:226-228)
+                cluster.join(r, cluster.side_event(r, entry[r], N * c, "intra_precompute", stream="compute2"))
+        else:
+            prevs_t, scanned_t = torch.zeros_like(finals), finals.clone()
         prevs = [None if (r == 0 and strategy is not StrategyKind.LASP2) else prevs_t[r] for r in range(P)]
         for r in range(P):
+            if strategy is not StrategyKind.ZECO:  # per rank: reduction, precompute, outputs (engine.py:275-279)
+                if strategy is StrategyKind.LASP2 and P > 1 and costs.per_state > 0.0:
+                    cluster.compute(r, math.log2(P) * costs.per_state, "state_reduce")
+                cluster.compute(r, N * c, "intra_precompute")
             with cluster.phase(r, "outputs"):
                 q, k, v, g = ranks[r]
                 outs.append(shards[r].fwd_output(q, k, v, g, prevs[r]))
+            cluster.compute(r, N * c, "outputs")
         prev_list = [prevs_t[r] for r in range(P)]
         final_list = [scanned_t[r] for r in range(P)]
         total_list = [totals[r] for r in range(P)]
@@ -214,13 +245,15 @@ def run_forward(seq: GlobalSequence, strategy: StrategyKind, cluster: DeviceClus
         for r in range(P):
             q, k, v, g = ranks[r]
             if r > 0:
-                cluster._count_received(r, "p2p", h * dk * dv)
+                cluster.p2p_recv(r, r - 1, primitive="p2p", label="recv:state")
             with cluster.phase(r, "rank_work"):
                 s_loc, g_tot = shards[r].fwd_local(k, v, g)
                 outs.append(shards[r].fwd_output(q, k, v, g, prev if r > 0 else None))
                 final = ops.global_correct(s_loc[None], g_tot[None], prev)[0]
+            for label in ("local_scan", "intra_precompute", "outputs"):
+                cluster.compute(r, N * c, label)
             if r < P - 1:
-                cluster._count_sent(r, "p2p", h * dk * dv)
+                cluster.p2p_send(r, r + 1, Payload(h * dk * dv), primitive="p2p", label="send:state")
             prev_list.append(prev)
             final_list.append(final)
             total_list.append(g_tot)
@@ -241,17 +274,23 @@ def run_forward(seq: GlobalSequence, strategy: StrategyKind, cluster: DeviceClus
         final_states=[State(back(f, npo)) for f in final_list],
         total_log_decays=[back(t, npo) for t in total_list],
         local_states=local_states,
-        _ctx={"shards": shards, "ranks": ranks, "prev": prev_list, "g_tot": total_list, "dtype": dt},
     )
     return RunArtifacts(outputs=back(o, npo, _np_dtype(seq)), ledger=cluster.read_ledger(),
                         timeline=cluster.read_timeline(), saved=saved,
-                        _bounds_fn=_boundary_fn(ranks, C, prev_list, npo))
+                        _bounds_fn=_boundary_fn(ranks, C, prev_list, npo),
+                        measured_timeline=cluster.read_measured_timeline())
 
 
-def run_backward(seq: GlobalSequence, d_out, strategy: StrategyKind, cluster: DeviceCluster | None,
+def run_backward(seq: GlobalSequence, d_out, strategy: StrategyKind, cluster: VirtualCluster | None,
                  pipe: PipelineConfig, saved_artifacts: RunArtifacts, costs: ComputeCosts = DEFAULT_COSTS
                  ) -> RunArtifacts:
-    """Distributed backward pass using state saved by run_forward (glasp/engine.py:301-420)."""
+    """Distributed backward pass using state saved by run_forward (glasp/engine.py:301-420).
+
+    Like the reference it reads the inputs from ``seq`` and the boundary values from the PUBLIC saved
+    fields (``prev_states``, ``total_log_decays``), so artifacts from any run_forward with the same
+    sequence work.  The per-rank local forward is re-run on the device first: the backward kernels walk
+    the forward's chunk states, which are recomputed from ``seq`` (the reference recomputes them from
+    prev too, glasp/gla.py:405-412)."""
     cluster = _check_cluster(seq, strategy, cluster)
     saved = saved_artifacts.saved
     if saved is None:
@@ -259,18 +298,28 @@ def run_backward(seq: GlobalSequence, d_out, strategy: StrategyKind, cluster: De
     if saved.strategy is not strategy:
         raise StateError(f"saved forward used {saved.strategy.value}, backward asked for {strategy.value}")
     P = 1 if strategy is StrategyKind.SINGLE_DEVICE else seq.num_ranks
+    if len(saved.prev_states) != P or len(saved.total_log_decays) != P:
+        raise StateError(f"saved forward holds {len(saved.prev_states)} ranks, this run has {P}")
     C = seq.layout.chunk_len
+    c = costs.per_chunk
+    N = seq.layout.num_chunks * (seq.num_ranks if strategy is StrategyKind.SINGLE_DEVICE else 1)
     npo = _is_numpy(seq)
     h, dk, dv = seq.dims.heads, seq.dims.key_dim, seq.dims.value_dim
-    ctx = saved._ctx
-    if ctx is None:
-        raise StateError("saved forward carries no device context (was it produced by this package?)")
-    ranks, shards, dt = ctx["ranks"], ctx["shards"], ctx["dtype"]
+    ranks, dt = _device_inputs(seq, P)
+    acc = acc_of(dt)
     L = ranks[0][0].shape[1]
+    if tuple(d_out.shape) != (h, P * L, dv):
+        raise DimsError(f"d_out has shape {tuple(d_out.shape)}, expected {(h, P * L, dv)}")
     dO = to_dev(d_out, dt)
     douts = [dO] if P == 1 else [dO[:, r * L:(r + 1) * L].contiguous() for r in range(P)]
-    totals = torch.stack(list(ctx["g_tot"]))
-    prevs = ctx["prev"]
+    prevs = [to_dev(st.values, acc) for st in saved.prev_states]
+    totals = torch.stack([to_dev(t, acc) for t in saved.total_log_decays])
+    shards = [ops.ZecoShard(h, L, dk, dv, C, dt) for _ in range(P)]
+    for r in range(P):  # the chunk states the backward kernels read (workspace of each rank's shard)
+        q, k, v, g = ranks[r]
+        shards[r].fwd_local(k, v, g)
+        if shards[r].fast:
+            shards[r].fwd_output(q, k, v, g, prevs[r] if r > 0 or strategy is StrategyKind.LASP2 else None)
     parts = [None] * P
 
     if strategy in (StrategyKind.ZECO, StrategyKind.SINGLE_DEVICE, StrategyKind.LASP2):
@@ -279,27 +328,39 @@ def run_backward(seq: GlobalSequence, d_out, strategy: StrategyKind, cluster: De
             with cluster.phase(r, "reverse_scan"):
                 q, k, v, g = ranks[r]
                 loc0.append(shards[r].bwd_local(q, g, douts[r]))
+            cluster.compute(r, N * c, "reverse_scan")
         loc0 = torch.stack(loc0)
+        entry = list(cluster.clocks)
         if strategy is StrategyKind.LASP2 and P > 1:
             from .collectives import all_gather_grouped
             all_gather_grouped(cluster, {"all_gather": list(loc0)})
             with cluster.phase(0, "state_reduce"):
                 ds_nexts, _ = ops.allscan_local(loc0, totals, 1, 1)
-        else:
+        elif strategy is StrategyKind.ZECO:
             ds_nexts, _ = all_scan_device(cluster, loc0, totals, pipe, ScanDirection.BWD)
+            for r in range(P):
+                cluster.join(r, cluster.side_event(r, entry[r], 2 * N * c, "grad_precompute", stream="compute2"))
+        else:
+            ds_nexts = torch.zeros_like(loc0)
         for r in range(P):
+            if strategy is not StrategyKind.ZECO:
+                if strategy is StrategyKind.LASP2 and P > 1 and costs.per_state > 0.0:
+                    cluster.compute(r, math.log2(P) * costs.per_state, "state_reduce")
+                cluster.compute(r, 2 * N * c, "grad_precompute")
             with cluster.phase(r, "grad_outputs"):
                 q, k, v, g = ranks[r]
                 first = r == 0 and strategy is not StrategyKind.LASP2
                 last = r == P - 1 and strategy is not StrategyKind.LASP2
                 parts[r] = shards[r].bwd_output(q, k, v, g, douts[r], None if first else prevs[r],
                                                 None if last else ds_nexts[r])
+            cluster.compute(r, N * c, "grad_outputs")
     elif strategy is StrategyKind.LASP1:
-        ds_next = torch.zeros((h, dk, dv), dtype=acc_of(dt), device=dO.device)
+        ds_next = torch.zeros((h, dk, dv), dtype=acc, device=dO.device)
         for r in range(P - 1, -1, -1):
             q, k, v, g = ranks[r]
             if r < P - 1:
-                cluster._count_received(r, "p2p", h * dk * dv)
+                cluster.p2p_recv(r, r + 1, primitive="p2p", label="recv:dstate")
+            cluster.compute(r, BACKWARD_PHASES * N * c, "rank_grad_work")
             with cluster.phase(r, "rank_grad_work"):
                 loc = shards[r].bwd_local(q, g, douts[r])
                 parts[r] = shards[r].bwd_output(q, k, v, g, douts[r], prevs[r] if r > 0 else None,
@@ -307,7 +368,7 @@ def run_backward(seq: GlobalSequence, d_out, strategy: StrategyKind, cluster: De
                 # ds_boundary = rev[0] + e^{G_tot} ds_next (glasp/gla.py:393-395)
                 ds_bound = ops.global_correct(loc[None], totals[r][None], ds_next)[0]
             if r > 0:
-                cluster._count_sent(r, "p2p", h * dk * dv)
+                cluster.p2p_send(r, r - 1, Payload(h * dk * dv), primitive="p2p", label="send:dstate")
             ds_next = ds_bound
     else:
         raise ConfigError(f"unsupported strategy {strategy}")
@@ -318,7 +379,8 @@ def run_backward(seq: GlobalSequence, d_out, strategy: StrategyKind, cluster: De
                       dg=back(cat(3), npo, nd))
     return RunArtifacts(outputs=saved_artifacts.outputs, ledger=cluster.read_ledger(),
                         timeline=cluster.read_timeline(), boundary_states=None, grads=grads, saved=saved,
-                        _bounds_fn=lambda: saved_artifacts.boundary_states)
+                        _bounds_fn=lambda: saved_artifacts.boundary_states,
+                        measured_timeline=cluster.read_measured_timeline())
 
 
 def ideal_makespan(strategy: StrategyKind, P: int, chunks_per_rank: int, costs: ComputeCosts = DEFAULT_COSTS,

@@ -99,15 +99,13 @@ class SeqShard:
     def dtype(self):
         return self.q.dtype
 
-    # device views used by the kernels (cached per shard)
     def device_tensors(self):
-        cache = getattr(self, "_dev", None)
-        if cache is None:
-            dt = compute_dtype(self.q)
-            acc = acc_of(dt)
-            cache = (to_dev(self.q, dt), to_dev(self.k, dt), to_dev(self.v, dt), to_dev(self.g, acc))
-            object.__setattr__(self, "_dev", cache)
-        return cache
+        """(q, k, v, g) on the device in the compute dtype.  Read from the arrays at every call (no cache):
+        the reference recomputes from the arrays each time, so in-place edits between calls must be seen.
+        Torch CUDA tensors of the compute dtype are used as they are (no copy)."""
+        dt = compute_dtype(self.q)
+        acc = acc_of(dt)
+        return to_dev(self.q, dt), to_dev(self.k, dt), to_dev(self.v, dt), to_dev(self.g, acc)
 
     @property
     def _numpy(self) -> bool:
@@ -201,7 +199,10 @@ def _np_dtype(shard):
 # ---------------------------------------------------------------- API
 
 def recurrent_forward(shard: SeqShard, init: State | None = None):
-    """Outputs, boundary states and final state from an optional initial state (glasp/gla.py:210-230)."""
+    """Token-by-token recurrence -> (outputs, N+1 boundary states, final) (glasp/gla.py:210-230).
+
+    Runs ``zgla_recurrent_forward`` (csrc/recurrence.cu): one state update per token, independent of
+    every chunkwise kernel, so it can arbitrate them as the reference's does."""
     q, k, v, g = shard.device_tensors()
     acc = acc_of(q.dtype)
     if init is not None:
@@ -209,12 +210,9 @@ def recurrent_forward(shard: SeqShard, init: State | None = None):
         if tuple(init.values.shape) != expected:
             raise DimsError(f"initial state has shape {tuple(init.values.shape)}, expected {expected}")
     init_d = None if init is None else to_dev(init.values, acc)
-    C = shard.layout.chunk_len
-    states, cum = ops.local_state_scan(k, v, g, C, init=init_d)
-    o = ops.forward_outputs(q, k, v, g, states, cum, None, C)
+    o, bounds, final = ops.recurrent_forward(q, k, v, g, shard.layout.chunk_len, init=init_d)
     npo = shard._numpy
-    bounds = _state_list(states, npo)
-    return back(o, npo, _np_dtype(shard)), bounds, State(back(states[-1].clone(), npo))
+    return back(o, npo, _np_dtype(shard)), _state_list(bounds, npo), State(back(final, npo))
 
 
 def chunk_scalings(g_chunk) -> ChunkScalings:
@@ -294,7 +292,11 @@ def backward(shard: SeqShard, d_out, prev: State, ds_next: State, saved_states=N
 
 
 def finite_diff_grad(shard: SeqShard, probe, step: float) -> GradShard:
-    """Central differences of <probe, recurrent_forward(shard)> (glasp/gla.py:447-480), float64 only."""
+    """Central differences of <probe, recurrent_forward(shard)> (glasp/gla.py:447-480), float64 only.
+
+    Every perturbed loss is a token recurrence (csrc/recurrence.cu ``fd_loss_kernel``, one CTA per
+    perturbation, one launch per tensor); grad[i] = (plus_i - minus_i) / (2 step) as in the reference.
+    States larger than the kernel's shared-memory budget take one ``recurrent_forward`` per perturbation."""
     if step <= 0.0:
         raise DomainError(f"step must be positive, got {step}")
     for name, arr in (("q", shard.q), ("k", shard.k), ("v", shard.v), ("g", shard.g), ("probe", probe)):
@@ -302,27 +304,31 @@ def finite_diff_grad(shard: SeqShard, probe, step: float) -> GradShard:
         if not (dt == np.float64 or dt == torch.float64):
             raise PrecisionError(f"{name} must be float64 for finite differences, got {dt}")
     npo = shard._numpy
+    base = [to_dev(getattr(shard, n), torch.float64) for n in ("q", "k", "v", "g")]
     pr = to_dev(probe, torch.float64)
-    base = {n: to_dev(getattr(shard, n), torch.float64).clone() for n in ("q", "k", "v", "g")}
-    C = shard.layout.chunk_len
-
-    def loss(t):
-        st, cm = ops.local_state_scan(t["k"], t["v"], t["g"], C)
-        o = ops.forward_outputs(t["q"], t["k"], t["v"], t["g"], st, cm, None, C)
-        return float((pr * o).sum().item())
-
+    h, ek, ev = shard.dims.heads, shard.dims.key_dim, shard.dims.value_dim
     grads = {}
-    for name in ("q", "k", "v", "g"):
-        x = base[name]
-        out = torch.zeros_like(x)
-        flat, oflat = x.view(-1), out.view(-1)
-        for i in range(flat.numel()):
-            orig = flat[i].item()
-            flat[i] = orig + step
-            plus = loss(base)
-            flat[i] = orig - step
-            minus = loss(base)
-            flat[i] = orig
-            oflat[i] = (plus - minus) / (2.0 * step)
-        grads[name] = back(out, npo)
+    for which, name in enumerate(("q", "k", "v", "g")):
+        if h * ek * ev <= ops.fd_max_state():
+            pm = ops.fd_losses(*base, pr, which, step).cpu().numpy()
+        else:
+            pm = _fd_losses_by_recurrence(base, pr, which, step, shard.layout.chunk_len)
+        grad = ((pm[:, 0] - pm[:, 1]) / (2.0 * step)).reshape(tuple(base[which].shape))
+        grads[name] = grad if npo else torch.from_numpy(grad).to(base[which].device)
     return GradShard(dq=grads["q"], dk=grads["k"], dv=grads["v"], dg=grads["g"])
+
+
+def _fd_losses_by_recurrence(base, probe, which, step, C):
+    x = base[which].clone()
+    flat = x.view(-1)
+    out = np.empty((flat.numel(), 2))
+    args = list(base)
+    args[which] = x
+    for i in range(flat.numel()):
+        orig = flat[i].item()
+        for col, bump in ((0, step), (1, -step)):
+            flat[i] = orig + bump
+            o, _, _ = ops.recurrent_forward(*args, C)
+            out[i, col] = float((probe * o).sum().item())
+        flat[i] = orig
+    return out

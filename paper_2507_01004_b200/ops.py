@@ -116,6 +116,43 @@ def check_log_decay(g: torch.Tensor) -> None:
         raise DomainError("log-decay entries must be strictly negative and finite")
 
 
+def recurrent_forward(q, k, v, g, C, init=None):
+    """glasp/gla.py:210-230: token-by-token recurrence -> (o [h,L,dv], bounds [N+1,h,dk,dv], final [h,dk,dv])."""
+    geo = geometry(q, v, C)
+    s = geo.shape()
+    q = _req(q, "q", geo.dtype, (geo.h, geo.L, geo.dk))
+    k = _req(k, "k", geo.dtype, (geo.h, geo.L, geo.dk))
+    v = _req(v, "v", geo.dtype, (geo.h, geo.L, geo.dv))
+    g = _req(g, "g", geo.acc, (geo.h, geo.L, geo.dk))
+    if init is not None:
+        init = _req(init, "init", geo.acc, (geo.h, geo.dk, geo.dv))
+    o = torch.empty((geo.h, geo.L, geo.dv), dtype=geo.dtype, device=q.device)
+    bounds = torch.empty((geo.N + 1, geo.h, geo.dk, geo.dv), dtype=geo.acc, device=q.device)
+    final = torch.empty((geo.h, geo.dk, geo.dv), dtype=geo.acc, device=q.device)
+    _native.call("zgla_recurrent_forward", ctypes.byref(s), _p(q), _p(k), _p(v), _p(g), _p(init), _p(o),
+                 _p(bounds), _p(final), _stream())
+    return o, bounds, final
+
+
+def fd_losses(q, k, v, g, probe, which: int, step: float):
+    """glasp/gla.py:463-480: sum(probe * recurrent_forward(x +/- step e_i)) for every element i of tensor
+    `which` (0 q, 1 k, 2 v, 3 g), float64 -> [numel, 2] (plus, minus); one kernel launch per tensor."""
+    h, L, dk = q.shape
+    dv = v.shape[2]
+    s = make_shape(h, L, dk, dv, 1, _native.ZGLA_F64)
+    ts = [_req(x, n, torch.float64, tuple(x.shape)) for x, n in ((q, "q"), (k, "k"), (v, "v"), (g, "g"))]
+    probe = _req(probe, "probe", torch.float64, (h, L, dv))
+    n = ts[which].numel()
+    losses = torch.empty((n, 2), dtype=torch.float64, device=q.device)
+    _native.call("zgla_fd_losses", ctypes.byref(s), *(_p(x) for x in ts), _p(probe), int(which), 0, 2 * n,
+                 float(step), _p(losses), _stream())
+    return losses
+
+
+def fd_max_state() -> int:
+    return int(_native.load().zgla_fd_max_state())
+
+
 def local_state_scan(k, v, g, C, init=None):
     """glasp/gla.py:248 (init: optional start state, as in recurrent_forward)."""
     geo = geometry(k, v, C)

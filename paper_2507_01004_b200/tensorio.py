@@ -30,7 +30,7 @@ def _to_numpy(values) -> np.ndarray:
 
 
 def encode_tensor(values) -> bytes:
-    arr = np.ascontiguousarray(_to_numpy(values), dtype="<f8")
+    arr = np.asarray(_to_numpy(values), dtype="<f8")  # (ascontiguousarray would lift a 0-d array to 1-d)
     if any(d >= 2 ** 32 for d in arr.shape):
         raise TensorFormatError(f"dimension too large for a u32 header: {arr.shape}")
     head = MAGIC + struct.pack("<I", arr.ndim) + struct.pack(f"<{arr.ndim}I", *arr.shape)
