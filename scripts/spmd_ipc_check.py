@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--seq", type=int, default=512, help="tokens per rank")
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--graph", action="store_true", help="capture fwd+bwd once as a CUDA graph and replay it")
+    ap.add_argument("--oracle", action="store_true",
+                    help="rank 0 also checks every output and gradient against the f64 CPU oracle (rtol 1e-2)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", 0 if args.same_device else int(os.environ.get("LOCAL_RANK", 0)))
@@ -86,6 +88,21 @@ def main():
             print(f"rank {p}: IPC All-Scan path {'bitwise equal to' if same else 'DIFFERS from'} the list form",
                   flush=True)
             assert same
+        if args.oracle:
+            sys.path.insert(0, ROOT)
+            import numpy as np
+            from oracle import gla_oracle as orc
+            f64 = lambda x: x.double().cpu().numpy()  # noqa: E731
+            qn, kn, vn, gn, don = f64(full[0]), f64(full[1]), f64(full[2]), f64(g_full), f64(do_full)
+            o_w, saved, _ = orc.zeco_forward(qn, kn, vn, gn, world, 64)
+            want, _ = orc.zeco_backward(qn, kn, vn, gn, don, world, 64, saved)
+            n = H * L * D
+            for i, (name, w) in enumerate(zip(("o", "dq", "dk", "dv", "dg"), (o_w,) + tuple(want))):
+                got = np.concatenate([gathered[p][i * n:(i + 1) * n].double().numpy().reshape(H, L, D)
+                                      for p in range(world)], axis=1)
+                err = orc.rel_err(got, w)
+                print(f"oracle {name}: rel err {err:.2e}", flush=True)
+                assert err <= 1e-2, (name, err)
         print(f"SPMD IPC check OK (P={world}, sent {comm.bytes_sent()} B on rank 0)", flush=True)
     dist.barrier()
     comm.close()

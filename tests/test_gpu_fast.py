@@ -287,3 +287,53 @@ def test_fast_domain_flag():
     g[1, 200, 7] = math.log(0.5)
     sh.fwd_local(k, v, g)  # the flag is per call
     sh.check_domain()
+
+
+@pytest.mark.parametrize("long_memory", [False, True])
+def test_fast_cfg1_full_size_seeds(long_memory):
+    """BASELINE config 1 at its stated size on the fused path: H=4, d=64, P=2 ranks x 2,048 tokens, K=4,
+    seeds 0..9, every output and gradient and the forward boundary states against the f64 oracle."""
+    worst = {}
+    for seed in range(10):
+        q, k, v, g, do = make_case(4, 2, 2048, seed=seed, long_memory=long_memory, D=64)
+        got = run_fast(q, k, v, g, do, 2, K=4)
+        want = oracle(q, k, v, g, do, 2)
+        errs = check(got, want)
+        errs["prev"] = rel(got["prev"], want["prev"])
+        assert errs["prev"] <= TOL_BF16
+        for kk, e in errs.items():
+            worst[kk] = max(worst.get(kk, 0.0), e)
+    print("cfg1 worst rel errors", {kk: f"{e:.2e}" for kk, e in worst.items()})
+
+
+@pytest.mark.parametrize("long_memory", [False, True])
+def test_fast_cfg2_more_heads_both_gates(long_memory):
+    """BASELINE config 2 (H=16, d=128, 16K tokens, 1 GPU): heads 0, 5, 10, 15 against the f64 oracle under
+    both gate distributions (the default and the long-memory one)."""
+    h, L = 16, 16384
+    q, k, v, g, do = make_case(h, 1, L, seed=21 + long_memory, long_memory=long_memory)
+    got = run_fast(q, k, v, g, do, 1)
+    for hh in (0, 5, 10, 15):
+        sl = slice(hh, hh + 1)
+        want = oracle(q[sl], k[sl], v[sl], g[sl], do[sl], 1)
+        check({kk: got[kk][sl] for kk in ("o", "dq", "dk", "dv", "dg")}, want)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_chunk_scalings_against_oracle(dtype):
+    """glasp/gla.py:233-245 chunk_scalings on the device: the reference's hand values (tests/test_gla.py:89-94)
+    and random chunks against the oracle; Lambda * Gamma = gamma."""
+    from paper_2507_01004_b200 import chunk_scalings
+    cs = chunk_scalings(np.log(np.array([[[0.5], [0.5]]], dtype=dtype)))
+    np.testing.assert_allclose(cs.chunk_decay, [[0.25]], rtol=1e-7)
+    np.testing.assert_allclose(cs.decay_from_start[0, :, 0], [0.5, 0.25], rtol=1e-7)
+    np.testing.assert_allclose(cs.decay_to_end[0, :, 0], [0.5, 1.0], rtol=1e-7)
+    rng = np.random.default_rng(4)
+    gch = rng.uniform(orc.DECAY_LOW, orc.DECAY_HIGH, (3, 64, 128)).astype(dtype)
+    cs = chunk_scalings(gch)
+    want = orc.chunk_scalings(gch.astype(np.float64))
+    tol = 1e-13 if dtype == np.float64 else 1e-6
+    for got, w in zip((cs.chunk_decay, cs.decay_from_start, cs.decay_to_end), want):
+        assert got.dtype == dtype and rel(got, w) <= tol
+    np.testing.assert_allclose(cs.decay_from_start * cs.decay_to_end,
+                               np.broadcast_to(cs.chunk_decay[:, None, :], gch.shape), rtol=1e-5 if dtype == np.float32 else 1e-14)

@@ -19,3 +19,16 @@ def test_ipc_allscan_two_processes_one_gpu(P, graph):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=400, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "SPMD IPC check OK" in r.stdout
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_ipc_cfg3_shape_against_oracle(P):
+    """BASELINE config 3 per-rank shape (16,384 tokens/rank, d=128; 2 heads, long-memory gates) through
+    ZecoRank / AllScanP2P in P processes, every output and gradient checked against the f64 oracle."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29641 + P),
+           os.path.join(ROOT, "scripts", "spmd_ipc_check.py"), "--same-device", "--rounds", "1",
+           "--seq", "16384", "--heads", "2", "--oracle"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "SPMD IPC check OK" in r.stdout and r.stdout.count("oracle ") == 5
