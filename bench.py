@@ -296,6 +296,93 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ N>1: All-Scan vs the baselines (same run)
+
+def _time_calls(fn, reps, use_graph, barrier, max_over_ranks):
+    """Mean device microseconds per fn() call: `reps` back-to-back calls captured in a CUDA graph (else
+    eager), after a warm-up; barrier + synchronize on both sides; max over ranks."""
+    import torch
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    graph, timed_as = None, "eager"
+    if use_graph:
+        try:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                fn()
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            barrier()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for _ in range(reps):
+                    fn()
+            graph.replay()
+            timed_as = "cuda_graph"
+        except Exception as e:  # a baseline that cannot be captured is timed eagerly
+            graph, timed_as = None, f"eager ({type(e).__name__} under capture)"
+            torch.cuda.synchronize()
+    samples = []
+    for _ in range(5):
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        if graph is not None:
+            graph.replay()
+        else:
+            for _ in range(reps):
+                fn()
+        b.record()
+        torch.cuda.synchronize()
+        samples.append(a.elapsed_time(b) * 1e3 / reps)
+    return max_over_ranks(statistics.median(samples)), timed_as
+
+
+def collective_bench(comm, H, D, K, dev, rank, world, same_device, barrier, max_over_ranks):
+    """BASELINE config 3's comparison in the bench run itself: the product All-Scan (in-kernel NVLink chain,
+    AllScanP2P) vs the NCCL send/recv chain (AllScanNCCL) vs the LASP-2 all-gather of states + reduction
+    (lasp2_states), on the layer's fp32 state [H, D, D]; plus a peer-copy bandwidth probe and tau_min."""
+    import torch
+    from paper_2507_01004_b200 import distributed as zd
+    gen = torch.Generator(device=dev).manual_seed(77 + rank)
+    s_loc = torch.rand((H, D, D), device=dev, generator=gen) * 2 - 1
+    g_tot = -2 * torch.rand((H, D), device=dev, generator=gen)
+    nccl = zd.AllScanNCCL()
+    use_graph = not same_device
+    res = {"state_bytes": H * D * D * 4, "K": K, "P": world}
+    res["p2p_us"], res["p2p_timed_as"] = _time_calls(lambda: comm(s_loc, g_tot, K, 0), 20, use_graph, barrier,
+                                                     max_over_ranks)
+    res["p2p_bwd_us"], _ = _time_calls(lambda: comm(s_loc, g_tot, K, 1), 20, use_graph, barrier, max_over_ranks)
+    res["nccl_chain_us"], res["nccl_chain_timed_as"] = _time_calls(lambda: nccl(s_loc, g_tot), 10, use_graph,
+                                                                   barrier, max_over_ranks)
+    res["allgather_states_us"], res["allgather_timed_as"] = _time_calls(lambda: zd.lasp2_states(s_loc, g_tot), 10,
+                                                                        use_graph, barrier, max_over_ranks)
+    res["allgather_over_allscan"] = res["allgather_states_us"] / res["p2p_us"]
+    res["tau_min_us"] = res["state_bytes"] / 900e9 * 1e6  # S / B_link, B_link = 900 GB/s per direction (spec)
+    res["nvlink_frac"] = res["tau_min_us"] / res["p2p_us"]
+    if not same_device and torch.cuda.device_count() > 1:  # measured peer copy rate rank -> rank + 1
+        peer = torch.device("cuda", (dev.index + 1) % torch.cuda.device_count())
+        src = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        dst = torch.empty(256 << 20, dtype=torch.uint8, device=peer)
+        for _ in range(2):
+            dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        gbs = 5 * src.numel() / (a.elapsed_time(b) / 1e3) / 1e9
+        res["p2p_copy_gbs"] = gbs
+        res["tau_measured_copy_us"] = res["state_bytes"] / (gbs * 1e9) * 1e6
+        del src, dst
+    return res
+
+
 # ------------------------------------------------------------------ GPU arm
 
 def main():
@@ -303,10 +390,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        if world > 1:
-            import torch.distributed as dist
-            dist.init_process_group("gloo")
+    if args.impl == "reference":  # CPU only; under torchrun rank 0 alone runs it, the others exit 0
         run_reference(args, rank, world)
         return
 
@@ -473,6 +557,7 @@ def main():
     step_bytes = (fwd_b + bwd_b) * units
     step_flops = (fwd_f + bwd_f) * units
 
+    shown = [p for p in phases if world > 1 or not p.endswith("_allscan")]  # no All-Scan at N=1
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -482,8 +567,8 @@ def main():
                    "allscan_blocks": args.blocks, "parallelism": f"zeco-sp{world}",
                    "l2": "inputs 384 MiB per GPU > 126 MiB L2 (no flush needed)"},
         "per_gpu_tokens_per_s": L / (ms_step / 1e3),
-        "phase_ms": {p: round(phase_timed[p], 5) for p in phases},  # graph-launched (event nodes between)
-        "phase_ms_eager": {p: round(per_phase[p], 5) for p in phases},
+        "phase_ms": {p: round(phase_timed[p], 5) for p in shown},  # graph-launched (event nodes between)
+        "phase_ms_eager": {p: round(per_phase[p], 5) for p in shown},
         "timed_as": "cuda_graph" if graph is not None else "eager",
         "roofline": {"kernel": {"fwd_output": "fwd_out_kernel", "bwd_output": "bwd_out_kernel",
                                 "fwd_local": "seg_state_kernel<0>+seg_scan_kernel<0>", "bwd_local": "seg_state_kernel<1>+seg_scan_kernel<1>"}[dom],
@@ -503,7 +588,11 @@ def main():
         "clocks": clk.summary(),
     }
     if world > 1:
-        line["allscan_us"] = {"fwd": per_phase["fwd_allscan"] * 1e3, "bwd": per_phase["bwd_allscan"] * 1e3}
+        # in-step chain time (event nodes around the All-Scan inside the captured step; includes the wait
+        # for the predecessors), then the isolated collective comparison of BASELINE config 3 / 4
+        line["allscan_in_step_us"] = {"fwd": phase_timed["fwd_allscan"] * 1e3, "bwd": phase_timed["bwd_allscan"] * 1e3}
+        line["allscan"] = collective_bench(comm, H, D, args.blocks, dev, rank, world, args.same_device,
+                                           dist.barrier, max_over_ranks)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_legs(H, D, C, 1024, 3, "repeat (3 repeats)")

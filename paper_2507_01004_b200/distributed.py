@@ -110,12 +110,17 @@ class AllScanNCCL:
     def __call__(self, local, log_decay, num_blocks=1, direction=0):
         order = list(range(self.world)) if direction == 0 else list(range(self.world - 1, -1, -1))
         pos = order.index(self.rank)
+        # gloo moves host tensors only (validation runs with every rank on one device)
+        host = local.is_cuda and dist.get_backend(self.group) == "gloo"
         recv = torch.zeros_like(local)
         if pos > 0:
-            dist.recv(recv, src=order[pos - 1], group=self.group)
+            buf = recv.cpu() if host else recv
+            dist.recv(buf, src=order[pos - 1], group=self.group)
+            if host:
+                recv.copy_(buf)
         scanned = _scan_update(log_decay, recv, local)
         if pos < self.world - 1:
-            dist.send(scanned, dst=order[pos + 1], group=self.group)
+            dist.send(scanned.cpu() if host else scanned, dst=order[pos + 1], group=self.group)
         return recv, scanned
 
 
@@ -128,9 +133,12 @@ def lasp2_states(local, log_decay, direction=0, group=None):
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(states, local.contiguous(), group=group)
         dist.all_gather_into_tensor(decays, log_decay.contiguous(), group=group)
-    else:  # gloo has no fused all-gather
-        dist.all_gather(list(states.unbind(0)), local.contiguous(), group=group)
-        dist.all_gather(list(decays.unbind(0)), log_decay.contiguous(), group=group)
+    else:  # gloo: no fused all-gather, host tensors
+        st_h, dc_h = states.cpu(), decays.cpu()
+        dist.all_gather(list(st_h.unbind(0)), local.contiguous().cpu(), group=group)
+        dist.all_gather(list(dc_h.unbind(0)), log_decay.contiguous().cpu(), group=group)
+        states.copy_(st_h)
+        decays.copy_(dc_h)
     order = list(range(world)) if direction == 0 else list(range(world - 1, -1, -1))
     recv = torch.zeros_like(local)
     for r in order:
