@@ -107,6 +107,11 @@ int zgla_fd_losses(const zgla_shape* s, const double* q, const double* k, const 
 int zgla_check_log_decay(long long n, int dtype, const void* g, int* bad_dev, void* stream);
 
 /* ---- ZeCO per-rank hot path (glasp/engine.py:218-237, 348-364) --------- */
+/* Early inputs (process-wide, off by default; returns the previous setting): the fused output kernels
+ * stream q / k / v / g / dO into shared memory before waiting for the kernel launched before them (the
+ * segment scan or the All-Scan chain), overlapping their prologue with it.  Caller contract: those
+ * tensors are complete before the matching zgla_zeco_*_local call is enqueued. */
+int zgla_set_early_inputs(int on);
 /* plan-dependent workspace for the four ZeCO entry points */
 long long zgla_zeco_workspace_bytes(const zgla_shape* s, int num_sms);
 /* local chunk scan: rank-local final state S_local [h][dk][dv] and total log decay G_tot [h][dk]

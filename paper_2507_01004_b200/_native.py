@@ -69,6 +69,7 @@ _SIGS = {
     "zgla_fd_max_state": ([], _LL),
     "zgla_fd_losses": ([ctypes.POINTER(Shape), _P, _P, _P, _P, _P, _I, _LL, _LL, ctypes.c_double, _P, _P], _I),
     "zgla_zeco_workspace_bytes": ([ctypes.POINTER(Shape), _I], _LL),
+    "zgla_set_early_inputs": ([_I], _I),
     "zgla_zeco_fwd_local": ([ctypes.POINTER(Shape), _I, _P, _P, _P, _P, _P, _P, _P], _I),
     "zgla_zeco_fwd_output": ([ctypes.POINTER(Shape), _I, _P, _P, _P, _P, _P, _P, _P, _P], _I),
     "zgla_zeco_bwd_local": ([ctypes.POINTER(Shape), _I, _P, _P, _P, _P, _P, _P], _I),

@@ -1,6 +1,8 @@
 // C ABI: library bookkeeping and the ZeCO per-rank entry points
 // (dispatch between the fused tcgen05 path and the generic validation path).
+#include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -11,6 +13,20 @@ namespace zgla {
 
 unsigned long long* g_trace_buf = nullptr;
 int g_trace_cta = 0;
+
+// early inputs of the fused output kernels (fast_common.cuh): process-wide caller contract, off by default
+static std::atomic<int> g_early_inputs{-1};
+namespace fast {
+int early_inputs() {
+  int v = g_early_inputs.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = std::getenv("ZGLA_EARLY_INPUTS");
+    v = (e && e[0] == '1') ? 1 : 0;
+    g_early_inputs.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+}  // namespace fast
 
 static thread_local char g_err[512] = "";
 
@@ -214,4 +230,10 @@ extern "C" int zgla_zeco_domain_check(const zgla_shape* s, int num_sms, const vo
     return ZGLA_ERR_DOMAIN;
   }
   return ZGLA_OK;
+}
+
+extern "C" int zgla_set_early_inputs(int on) {
+  const int old = zgla::fast::early_inputs();
+  zgla::g_early_inputs.store(on ? 1 : 0, std::memory_order_relaxed);
+  return old;
 }

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
                    const float* __restrict__ Dend, const float* __restrict__ cumGr,
                    const float* __restrict__ ds_next, __nv_bfloat16* __restrict__ dq, __nv_bfloat16* __restrict__ dk,
                    __nv_bfloat16* __restrict__ dv, float* __restrict__ dg, Strides4 gs, unsigned long long* trace,
-                   int trace_cta) {
+                   int trace_cta, int early) {
   extern __shared__ uint8_t smem_raw[];
   // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -131,13 +131,9 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   // under a programmatic (PDL) launch every warp waits for the preceding grid before touching memory;
-  // ZGLA_EARLY: only the epilogue warps, whose prologue reads the preceding scan's outputs (Dend, cumGr)
+  // early inputs: only the epilogue warps, whose prologue reads the preceding scan's outputs (Dend, cumGr)
   pdl_trigger();
-#if ZGLA_EARLY
-  if (warp < 8) pdl_wait();  // the other warps stream inputs the preceding kernel did not write
-#else
-  pdl_wait();
-#endif
+  if (!early || warp < 8) pdl_wait();  // early: the other warps stream inputs the preceding kernel did not write
 
   if (warp == 12) {
     // ---------------- TMA producer (tiles right to left)
@@ -164,6 +160,9 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d, pol);
         tile_load<DENSE>(sb + 3 * TILE_BF16, &tm_do, &full[st], 0, r, hh, L, in3d, pol);
         tile_load<DENSE>(sb + 3 * TILE_BF16 + PANEL, &tm_do, &full[st], 64, r, hh, L, in3d, pol);
+        // S' comes from the forward output kernel three launches back: with early inputs this lane waits
+        // for the preceding grid (whose completion implies every earlier one's) before its first S' load
+        if (m == 0 && early) pdl_wait();
         mbar_wait(sp_empty, (m & 1) ^ 1);
         if (dr == D) {
           mbar_arrive_expect_tx(sp_full, STATE_BF16);
@@ -531,12 +530,13 @@ int fast_bwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   const Strides4 gs{(int)dq.ts, (int)dk.ts, (int)dv.ts, (int)dg.ts, dq.hs, dk.hs, dv.hs, dg.hs};
   auto kern = dn ? bwd_out_kernel<true> : bwd_out_kernel<false>;
   set_smem_once((const void*)kern, (int)BO_SMEM);
-  if (cudaError_t e = launch_kp(ZGLA_EARLY || pdl_enabled(), kern, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp, mg,
+  const int early = pdl_enabled() && early_inputs();
+  if (cudaError_t e = launch_kp(pdl_enabled(), kern, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp, mg,
                                 (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
                                 (const float*)w.Sin, (const float*)w.cumG, (const float*)w.dS, (const float*)w.gam, (const float*)s_prev,
                                 (const float*)w.Dend, (const float*)w.cumGr, (const float*)ds_next,
                                 (__nv_bfloat16*)dq.p, (__nv_bfloat16*)dk.p, (__nv_bfloat16*)dv.p, (float*)dg.p, gs,
-                                g_trace_buf, g_trace_cta))
+                                g_trace_buf, g_trace_cta, early))
     return cuda_fail(e, "bwd_out_kernel");
   return zgla_check_launch();
 }

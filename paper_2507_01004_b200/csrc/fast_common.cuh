@@ -279,7 +279,7 @@ inline void set_smem_once(const void* fn, int bytes) {
 // ---- launches with programmatic dependent launch (PDL): a kernel's CTAs become resident as the
 // previous kernel's CTAs retire and run their prologue (barrier init, TMEM alloc, descriptor
 // prefetch) before griddepcontrol.wait releases them.  Every warp of every fused kernel waits before
-// its first global access (unless compiled with ZGLA_EARLY), and a grid completes only after its own
+// its first global access (unless early inputs are enabled), and a grid completes only after its own
 // wait, so all memory of the kernels before it is visible.  On by default (ZGLA_PDL=0 turns it off):
 // on the final kernels the CUDA-graph step is 0.3649-0.3660 -> 0.3630-0.3637 ms (round-1 kernels:
 // 0.3945 -> 0.400, then it was opt-in).
@@ -306,9 +306,12 @@ inline cudaError_t launch_kp(bool pdl, void (*kern)(Exp...), dim3 grid, dim3 blo
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
-#ifndef ZGLA_EARLY
-#define ZGLA_EARLY 0
-#endif
+// Early inputs (zgla_set_early_inputs): the output kernels' TMA and prep warps read q / k / v / g / dO
+// before griddepcontrol.wait, so they stream under the preceding kernel (the segment scan, or the All-Scan
+// chain when there are peers).  A caller contract: those tensors must be complete before the matching
+// zgla_zeco_*_local call is enqueued (true for ZecoRank, the GLA layer and bench.py; not for a caller
+// that writes q or dO in its own programmatic-launch kernel right before an output call).  Off by default.
+int early_inputs();
 template <typename... Exp, typename... Act>
 inline cudaError_t launch_k(void (*kern)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                             Act&&... args) {

@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
                    const float* __restrict__ Sin,
                    const float* __restrict__ cumG, const float* __restrict__ s_prev,
                    __nv_bfloat16* __restrict__ out, long long ots, long long ohs,
-                   __nv_bfloat16* __restrict__ sp_save, unsigned long long* trace, int trace_cta) {
+                   __nv_bfloat16* __restrict__ sp_save, unsigned long long* trace, int trace_cta, int early) {
   extern __shared__ uint8_t smem_raw[];
   // align by offsetting the __shared__ array itself so the compiler keeps the shared address space (LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -346,11 +346,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   // Only the state warps read the preceding scan's outputs (Sin, cumG): with an early launch the
   // loads of q / k / v / g and the per-tile prep run while that kernel is still finishing.
   pdl_trigger();
-#if ZGLA_EARLY
-  if (warp < 4) pdl_wait();  // the other warps stream inputs the preceding kernel did not write
-#else
-  pdl_wait();
-#endif
+  if (!early || warp < 4) pdl_wait();  // early: the other warps stream inputs the preceding kernel did not write
 
   if (warp == 12) {
     // ---------------- TMA producer
@@ -761,11 +757,12 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
     if (int rc = map_act(&mo, o, pl.L, pl.h, true)) return rc;
   auto kern = dn ? fwd_out_kernel<true> : fwd_out_kernel<false>;
   set_smem_once((const void*)kern, (int)FO_SMEM);
-  if (cudaError_t e = launch_kp(ZGLA_EARLY || pdl_enabled(), kern, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
+  const int early = pdl_enabled() && early_inputs();
+  if (cudaError_t e = launch_kp(pdl_enabled(), kern, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
                                 mo, (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
                                 (const float*)w.Sin, (const float*)w.cumG, (const float*)s_prev, (__nv_bfloat16*)o.p,
                                 o.ts, o.hs, w.Sp,
-                                g_trace_buf, g_trace_cta))
+                                g_trace_buf, g_trace_cta, early))
     return cuda_fail(e, "fwd_out_kernel");
   return zgla_check_launch();
 }

@@ -151,8 +151,11 @@ def lasp2_states(local, log_decay, direction=0, group=None):
 class ZecoRank:
     """One rank of ZeCO sequence-parallel GLA (one layer, fwd + bwd) over ``comm``."""
 
-    def __init__(self, heads, seq_len, dim, chunk_len=64, dtype=torch.bfloat16, comm=None, num_blocks=4, sms=None):
+    def __init__(self, heads, seq_len, dim, chunk_len=64, dtype=torch.bfloat16, comm=None, num_blocks=4, sms=None,
+                 early_inputs=True):
         self.shard = ops.ZecoShard(heads, seq_len, dim, dim, chunk_len, dtype, sms=sms)
+        if early_inputs:  # forward()/backward() take every input at once: the early-input contract holds
+            _native.load().zgla_set_early_inputs(1)
         self.comm = comm
         self.K = num_blocks
         self.world = comm.world if comm is not None else 1

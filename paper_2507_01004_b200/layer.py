@@ -8,8 +8,8 @@ this module is the wrapper a training stack needs around the hot path:
   All-Scan FWD -> outputs with the fused correction; local reverse scan ->
   All-Scan BWD -> gradients with the fused corrections.  Tensors are
   ``[h, L, d]`` (the reference layout, glasp/gla.py:29-30) and may be strided views of
-  token-major buffers (zgla_tensor strides, no transposing copies); the per-call ZecoShard workspace (segment states, saved chunk states) is kept
-  on the autograd context from forward to backward.
+  token-major buffers (zgla_tensor strides, no transposing copies); the per-call ZecoShard workspace (segment
+  states, saved chunk states) is a saved tensor, so activation recompute drops and regenerates it.
 * ``GatedLinearAttention`` -- hidden -> q, k, v, r (one GEMM; the kernels read its head slices in place),
   low-rank log-sigmoid gate (g < 0 by construction), ZeCO GLA core, per-head
   RMS norm, swish output gate, output projection.
@@ -59,28 +59,32 @@ class ZecoGLAFunction(torch.autograd.Function):
         # surrounding GEMMs consume: the runtime-stride kernel variant costs ~10 % of the core
         # (scripts/strided_bench.py) but saves the transposing copies (GLA-1.3B step 2.06 -> 1.87 s)
         o = shard.fwd_output(q, k, v, g, prev, out=_token_major(h, L, dv, q.dtype, q.device))
-        ctx.save_for_backward(q, k, v, g)
-        ctx.shard, ctx.prev, ctx.g_tot = shard, prev, g_tot
+        # everything the backward needs goes through save_for_backward -- including the shard's workspace
+        # (segment states, saved chunk states) -- so activation checkpointing can drop and regenerate it
+        none = torch.empty(0, device=q.device)
+        ctx.save_for_backward(q, k, v, g, shard.ws, g_tot, prev if prev is not None else none)
+        ctx.geom = (h, L, dk, dv, chunk_len, q.dtype, shard.sms)
         ctx.comm, ctx.K, ctx.world, ctx.rank = comm, num_blocks, world, rank
         return o
 
     @staticmethod
     def backward(ctx, d_out):
-        q, k, v, g = ctx.saved_tensors
-        shard = ctx.shard
+        q, k, v, g, ws, g_tot, prev = ctx.saved_tensors
+        h, L, dk, dv, C, dt, sms = ctx.geom
+        shard = ops.ZecoShard(h, L, dk, dv, C, dt, device=q.device, sms=sms, ws=ws)
+        prev = prev if prev.numel() else None
         d_out = d_out.to(q.dtype)
         if d_out.stride(2) != 1:
             d_out = d_out.contiguous()
         ds0 = shard.bwd_local(q, g, d_out)
         ds_next = None
         if ctx.world > 1:
-            recv, _ = ctx.comm(ds0, ctx.g_tot, ctx.K, _native.ZGLA_BWD)
+            recv, _ = ctx.comm(ds0, g_tot, ctx.K, _native.ZGLA_BWD)
             ds_next = recv if ctx.rank < ctx.world - 1 else None
         h, L, dk_, dv_ = q.shape[0], q.shape[1], q.shape[2], v.shape[2]
         grads = (_token_major(h, L, dk_, q.dtype, q.device), _token_major(h, L, dk_, q.dtype, q.device),
                  _token_major(h, L, dv_, q.dtype, q.device), _token_major(h, L, dk_, g.dtype, q.device))
-        dq, dk, dv, dg = shard.bwd_output(q, k, v, g, d_out, ctx.prev, ds_next, grads=grads)
-        ctx.shard = None
+        dq, dk, dv, dg = shard.bwd_output(q, k, v, g, d_out, prev, ds_next, grads=grads)
         return dq, dk, dv, dg, None, None, None
 
 

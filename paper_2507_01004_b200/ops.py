@@ -281,7 +281,9 @@ class ZecoShard:
     four ZeCO entry points of the C ABI.
     """
 
-    def __init__(self, heads, seq_len, key_dim, value_dim, chunk_len, dtype, device=None, sms=None):
+    def __init__(self, heads, seq_len, key_dim, value_dim, chunk_len, dtype, device=None, sms=None, ws=None):
+        """``ws``: adopt an existing workspace (e.g. one saved for backward by an autograd Function) instead
+        of allocating one; such a shard does not register the lazy domain watch."""
         self.geo = Geometry(heads, seq_len, key_dim, value_dim, chunk_len, dtype)
         self.shape = self.geo.shape()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -289,10 +291,12 @@ class ZecoShard:
         nbytes = _native.load().zgla_zeco_workspace_bytes(ctypes.byref(self.shape), self.sms)
         if nbytes < 0:
             raise DimsError("invalid ZeCO shard geometry")
-        self.ws = _ws(nbytes, self.device)
+        if ws is not None and (ws.dtype != torch.uint8 or ws.numel() < nbytes or not ws.is_cuda):
+            raise DimsError(f"adopted workspace must be a CUDA uint8 tensor of >= {nbytes} bytes")
+        self.ws = _ws(nbytes, self.device) if ws is None else ws
         self.fast = bool(_native.load().zgla_fast_path(ctypes.byref(self.shape)))
         self._dom = None
-        if self.fast:  # lazy domain reports of the fused forward segment pass (host-mapped word)
+        if self.fast and ws is None:  # lazy domain reports of the fused forward segment pass (host-mapped word)
             dom = ctypes.POINTER(ctypes.c_int)()
             _native.call("zgla_zeco_watch_domain", _p(self.ws), ctypes.byref(dom))
             self._dom = dom

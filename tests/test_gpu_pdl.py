@@ -49,8 +49,8 @@ print(eager, digest())
 """
 
 
-def run(pdl):
-    env = dict(os.environ, ZGLA_PDL=pdl)
+def run(pdl, early="0"):
+    env = dict(os.environ, ZGLA_PDL=pdl, ZGLA_EARLY_INPUTS=early)
     out = subprocess.run([sys.executable, "-c", SCRIPT, ROOT], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     return out.stdout.split()[-2:]
@@ -61,3 +61,11 @@ def test_pdl_launch_is_bit_identical():
     assert on[0] == on[1], "graph replay differs from the eager step (PDL on)"
     assert off[0] == off[1], "graph replay differs from the eager step (PDL off)"
     assert on == off
+
+
+def test_early_inputs_bit_identical():
+    """Early inputs (the output kernels stream q/k/v/g/dO before waiting for the preceding grid) change only
+    the launch overlap, never the results."""
+    early, plain = run("1", "1"), run("1", "0")
+    assert early[0] == early[1], "graph replay differs from the eager step (early inputs)"
+    assert early == plain
