@@ -17,6 +17,7 @@ reference's VolumeLedger contract.
 from __future__ import annotations
 
 import ctypes
+import os
 from collections import defaultdict
 
 import torch
@@ -154,7 +155,9 @@ class ZecoRank:
     def __init__(self, heads, seq_len, dim, chunk_len=64, dtype=torch.bfloat16, comm=None, num_blocks=4, sms=None,
                  early_inputs=True):
         self.shard = ops.ZecoShard(heads, seq_len, dim, dim, chunk_len, dtype, sms=sms)
-        if early_inputs:  # forward()/backward() take every input at once: the early-input contract holds
+        # forward()/backward() take every input at once, so the early-input contract holds (ZGLA_EARLY_INPUTS=0
+        # in the environment keeps it off, for A/B runs)
+        if early_inputs and os.environ.get("ZGLA_EARLY_INPUTS", "1") != "0":
             _native.load().zgla_set_early_inputs(1)
         self.comm = comm
         self.K = num_blocks

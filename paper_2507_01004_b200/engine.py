@@ -23,7 +23,7 @@ from . import ops
 from ._convert import acc_of, back, compute_dtype, to_dev
 from .cluster import NetConfig, Payload, VirtualCluster, VirtualTimeline, VolumeLedger, create_cluster
 from .collectives import PipelineConfig, ScanDirection, all_scan_device
-from .errors import ConfigError, DimsError, LayoutError, StateError
+from .errors import ConfigError, DimsError, DomainError, LayoutError, StateError
 from .gla import CumDecay, GradShard, ModelDims, SeqShard, ShardLayout, State
 
 
@@ -179,6 +179,39 @@ def _boundary_fn(ranks, C, prevs, npo):
     return build
 
 
+def _local_scans(cluster, shards, ranks):
+    """Each rank's local scan (K1 + K2), or None when a fused-path shard saw a 64-token tile whose summed
+    log-decay leaves its exponent domain."""
+    loc = []
+    for r, (sh, (q, k, v, g)) in enumerate(zip(shards, ranks)):
+        if cluster is not None:
+            with cluster.phase(r, "local_scan"):
+                loc.append(sh.fwd_local(k, v, g))
+        else:
+            loc.append(sh.fwd_local(k, v, g))
+    for sh in shards:
+        if sh.fast:
+            try:
+                sh.check_domain()
+            except DomainError:
+                return None
+    return loc
+
+
+def _widened(fn, seq, *args):
+    """Run ``fn`` on an fp32 copy of a bf16 sequence (the SIMT kernels use the exact token recurrence and
+    accept every gate the reference accepts) and hand back bf16 tensors like the fused path would."""
+    wide = GlobalSequence(q=seq.q.float(), k=seq.k.float(), v=seq.v.float(), g=seq.g, num_ranks=seq.num_ranks,
+                          layout=seq.layout, dims=seq.dims)
+    args = [a.float() if isinstance(a, torch.Tensor) and a.dtype == torch.bfloat16 else a for a in args]
+    art = fn(wide, *args)
+    cast = (lambda t: t.to(torch.bfloat16) if isinstance(t, torch.Tensor) and t.dtype == torch.float32 else t)
+    art.outputs = cast(art.outputs)
+    if art.grads is not None:
+        art.grads = GradShard(dq=cast(art.grads.dq), dk=cast(art.grads.dk), dv=cast(art.grads.dv), dg=art.grads.dg)
+    return art
+
+
 def run_forward(seq: GlobalSequence, strategy: StrategyKind, cluster: VirtualCluster | None,
                 pipe: PipelineConfig = PipelineConfig(), costs: ComputeCosts = DEFAULT_COSTS,
                 save_all: bool = False) -> RunArtifacts:
@@ -200,17 +233,14 @@ def run_forward(seq: GlobalSequence, strategy: StrategyKind, cluster: VirtualClu
     shards = [ops.ZecoShard(h, L, dk, dv, C, dt) for _ in range(P)]
     zero = torch.zeros((h, dk, dv), dtype=acc, device=ranks[0][0].device)
     outs = []
+    pre = _local_scans(cluster, shards, ranks)
+    if pre is None:  # a gate outside the fused bf16 path's exponent domain: the fp32 kernels take any gate
+        return _widened(run_forward, seq, strategy, cluster, pipe, costs, save_all)
 
     if strategy in (StrategyKind.ZECO, StrategyKind.SINGLE_DEVICE, StrategyKind.LASP2):
-        loc = []
+        loc = pre
         for r in range(P):
-            with cluster.phase(r, "local_scan"):
-                q, k, v, g = ranks[r]
-                loc.append(shards[r].fwd_local(k, v, g))
             cluster.compute(r, N * c, "local_scan")
-        for sh in shards:  # the fused bf16 path's exponent domain (DomainError, like invalid gates)
-            if sh.fast:
-                sh.check_domain()
         finals = torch.stack([x[0] for x in loc])
         totals = torch.stack([x[1] for x in loc])
         entry = list(cluster.clocks)
@@ -315,9 +345,10 @@ def run_backward(seq: GlobalSequence, d_out, strategy: StrategyKind, cluster: Vi
     prevs = [to_dev(st.values, acc) for st in saved.prev_states]
     totals = torch.stack([to_dev(t, acc) for t in saved.total_log_decays])
     shards = [ops.ZecoShard(h, L, dk, dv, C, dt) for _ in range(P)]
+    if _local_scans(None, shards, ranks) is None:  # same widening as the forward
+        return _widened(run_backward, seq, d_out, strategy, cluster, pipe, saved_artifacts, costs)
     for r in range(P):  # the chunk states the backward kernels read (workspace of each rank's shard)
         q, k, v, g = ranks[r]
-        shards[r].fwd_local(k, v, g)
         if shards[r].fast:
             shards[r].fwd_output(q, k, v, g, prevs[r] if r > 0 or strategy is StrategyKind.LASP2 else None)
     parts = [None] * P

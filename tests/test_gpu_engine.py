@@ -127,3 +127,22 @@ def test_engine_bf16_fast_path_long_memory():
     assert rel(f(art.outputs), o) <= TOL_BF16
     for got, want in ((grads.dq, dq), (grads.dk, dk), (grads.dv, dv), (grads.dg, dg)):
         assert rel(f(got), want) <= TOL_BF16
+
+
+def test_engine_bf16_any_gate_the_reference_accepts():
+    """Gates far outside the fused path's exponent domain (per-token decay 0.02-0.05: a 64-token tile's
+    log-decay near -200) are accepted by the drop-in engine like the reference accepts them: the call
+    widens to the fp32 kernels (exact token recurrence) and returns bf16 outputs/gradients."""
+    seq = make_seq(41, P=2, L=256, C=64, h=2, ek=128, ev=128, precision="bf16",
+                   decay_low=math.log(0.02), decay_high=math.log(0.05))
+    do = torch.rand(2, 2 * 256, 128, device="cuda", dtype=torch.float32).mul(2).sub(1).to(torch.bfloat16)
+    art, cl = fwd(seq, "ZECO", K=4)
+    grads = bwd(seq, do, "ZECO", art, cl, K=4).grads
+    assert art.outputs.dtype == torch.bfloat16 and grads.dq.dtype == torch.bfloat16
+    f = lambda t: t.double().cpu().numpy()  # noqa: E731
+    q, k, v, g = f(seq.q), f(seq.k), f(seq.v), f(seq.g)
+    o, saved, _ = orc.zeco_forward(q, k, v, g, 2, 64)
+    (dq, dk, dv, dg), _ = orc.zeco_backward(q, k, v, g, f(do), 2, 64, saved)
+    assert rel(f(art.outputs), o) <= TOL_BF16
+    for got, want in ((grads.dq, dq), (grads.dk, dk), (grads.dv, dv), (grads.dg, dg)):
+        assert rel(f(got), want) <= TOL_BF16
