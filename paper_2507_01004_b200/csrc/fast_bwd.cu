@@ -43,8 +43,17 @@ constexpr size_t BO_SMEM = 1024 + BO_OFF_BAR + 256;
 // TMEM columns.  Scores (lanes 0-15 of each quarter) and dP (lanes 16-31) share one M=64 column block;
 // LB holds d = logb - r per (channel lane, token column), double buffered, written by the prep warps.
 constexpr uint32_t BC_DQ = 0, BC_DK = 64, BC_DV = 128, BC_QDO = 192, BC_SC = 320, BC_LB = 384;
+// PAIR (d = 64, heads 2*hh / 2*hh+1 on channels 0-63 / 64-127): every accumulator whose rows are channels
+// is split per head into two M = 64 MMAs that fill the two lane halves of each TMEM lane quarter, so TMEM
+// lane l = 32*qd + 16*e + x holds channel c = 64*e + 16*qd + x of head e (pair_channel).  Dt shrinks to
+// 64 columns (its cross-head blocks are never formed), which frees BC_SC2 for the second head's scores.
+// The second head's masked operands live in the unused off-diagonal blocks of the S' buffer.
+constexpr uint32_t BC_SC2 = 256;
+__device__ __forceinline__ int pair_channel(int lane_id) {  // TMEM lane (0..127) -> channel of the pair
+  return 64 * ((lane_id & 31) >> 4) + 16 * (lane_id >> 5) + (lane_id & 15);
+}
 
-template <bool DENSE>
+template <bool DENSE, bool PAIR = false>
 __global__ void __launch_bounds__(BO_THREADS, 1)
     bwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
@@ -93,10 +102,11 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   const int nt = t1 - t0;
   unsigned long long* tr = (trace != nullptr && (int)blockIdx.x == trace_cta) ? trace : nullptr;
   if (trace != nullptr && threadIdx.x == 0) cta_trace_begin(trace);
+  constexpr int DW = PAIR ? 64 : D;  // channels per head in memory
   if constexpr (DENSE) {  // compile-time strides for the dense layout
-    gts = D, ghs = L * D;
-    gs = Strides4{D, D, D, D, L * D, L * D, L * D, L * D};
-    dr = D;
+    gts = DW, ghs = L * DW;
+    gs = Strides4{DW, DW, DW, DW, L * DW, L * DW, L * DW, L * DW};
+    dr = DW;
   }
 
   if (tid == 0) {
@@ -118,7 +128,9 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
     mbar_init(&lb_empty[1], 256);
     fence_barrier_init();
   }
-  if (dr < D) {  // d = 64: S' tiles fill only the top-left 64 x 64 block of this buffer
+  uint8_t* am1_buf = sp_buf + T * 128;  // PAIR: S' panel 0 rows 64-127
+  uint8_t* dpm1_buf = sp_buf + SPANEL;   // PAIR: S' panel 1 rows 0-63
+  if (!PAIR && dr < D) {  // d = 64: S' tiles fill only the top-left 64 x 64 block of this buffer
     for (int i = tid; i < STATE_BF16 / 16; i += BO_THREADS) reinterpret_cast<uint4*>(sp_buf)[i] = make_uint4(0, 0, 0, 0);
     fence_proxy_async();
   }
@@ -152,19 +164,32 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], BO_STAGE);
         const int r = n * T;
-        tile_load<DENSE>(sb, &tm_q, &full[st], 0, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + PANEL, &tm_q, &full[st], 64, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + TILE_BF16, &tm_k, &full[st], 0, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + 3 * TILE_BF16, &tm_do, &full[st], 0, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + 3 * TILE_BF16 + PANEL, &tm_do, &full[st], 64, r, hh, L, in3d, pol);
+        if constexpr (PAIR) {
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const CUtensorMap* mx = x == 0 ? &tm_q : x == 1 ? &tm_k : x == 2 ? &tm_v : &tm_do;
+            tile_load<false>(sb + x * TILE_BF16, mx, &full[st], 0, r, 2 * hh, L, 1, pol);
+            tile_load<false>(sb + x * TILE_BF16 + PANEL, mx, &full[st], 0, r, 2 * hh + 1, L, 1, pol);
+          }
+        } else {
+          tile_load<DENSE>(sb, &tm_q, &full[st], 0, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + PANEL, &tm_q, &full[st], 64, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + TILE_BF16, &tm_k, &full[st], 0, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + 3 * TILE_BF16, &tm_do, &full[st], 0, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + 3 * TILE_BF16 + PANEL, &tm_do, &full[st], 64, r, hh, L, in3d, pol);
+        }
         // S' comes from the forward output kernel three launches back: with early inputs this lane waits
         // for the preceding grid (whose completion implies every earlier one's) before its first S' load
         if (m == 0 && early) pdl_wait();
         mbar_wait(sp_empty, (m & 1) ^ 1);
-        if (dr == D) {
+        if constexpr (PAIR) {  // the two per-head blocks onto the diagonal of the [c][v] buffer
+          mbar_arrive_expect_tx(sp_full, 2 * T * 128);
+          tma_load_2d(sp_buf, &tm_sp, sp_full, 0, ((2 * hh) * ntiles + n) * 64);
+          tma_load_2d(sp_buf + SPANEL + T * 128, &tm_sp, sp_full, 0, ((2 * hh + 1) * ntiles + n) * 64);
+        } else if (dr == D) {
           mbar_arrive_expect_tx(sp_full, STATE_BF16);
           const int rs = (hh * ntiles + n) * D;
           tma_load_2d(sp_buf, &tm_sp, sp_full, 0, rs);
@@ -177,8 +202,14 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         // warm L2 with the gate tile the prep warps read (pointer loads) ZGLA_G_PREFETCH tiles from now
         if (n - ZGLA_G_PREFETCH >= t0) {
           const int rg = (n - ZGLA_G_PREFETCH) * T;
-          if (in3d) tma_prefetch_3d(&tm_g, 0, rg, hh);
-          else tma_prefetch_2d(&tm_g, 0, (int)(hh * L + rg));
+          if constexpr (PAIR) {
+            tma_prefetch_3d(&tm_g, 0, rg, 2 * hh);
+            tma_prefetch_3d(&tm_g, 0, rg, 2 * hh + 1);
+          } else if (in3d) {
+            tma_prefetch_3d(&tm_g, 0, rg, hh);
+          } else {
+            tma_prefetch_2d(&tm_g, 0, (int)(hh * L + rg));
+          }
         }
 #endif
         ZTRACE(tr, 0, m);
@@ -192,20 +223,38 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       constexpr uint32_t id_mk = idesc_bf16(128, 64, true, false);
       constexpr uint32_t id_kk = idesc_bf16(128, 64, false, false);
       constexpr uint32_t id_mm = idesc_bf16(128, 64, true, true);
+      // PAIR: per-head M = 64 shapes
+      constexpr uint32_t id_mk64 = idesc_bf16(64, 64, true, false);
+      constexpr uint32_t id_kk64 = idesc_bf16(64, 64, false, false);
+      constexpr uint32_t id_mm64 = idesc_bf16(64, 64, true, true);
       const uint32_t spa = smem_u32(sp_buf), dpa = smem_u32(dp_buf);
       const uint32_t ama = smem_u32(am_buf), dpma = smem_u32(dpm_buf);
+      const uint32_t am_e[2] = {ama, smem_u32(am1_buf)}, dpm_e[2] = {dpma, smem_u32(dpm1_buf)};
       for (int m = 0; m < nt; ++m) {
         const int st = m % BO_NS, ph = (m / BO_NS) & 1;
         const uint32_t qa = smem_u32(smem + st * BO_STAGE);
         const uint32_t ka = qa + TILE_BF16, va = qa + 2 * TILE_BF16, da = qa + 3 * TILE_BF16;
         mbar_wait(&prep[st], ph);
         tc_fence_after();
+        if constexpr (PAIR) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {  // scores and dP, K = 128 channels
-          const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
-          mma_bf16_ss(tbase + BC_SC, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_sc, kk > 0);
-          mma_bf16_ss(tbase + (16u << 16) + BC_SC, sdesc(da + off, 16, 1024), sdesc(va + off, 16, 1024), id_sc,
-                      kk > 0);
+          for (int e = 0; e < 2; ++e) {  // scores / dP of head e (K = its 64 channels) in lane half e
+            const uint32_t lo = (16u * e) << 16;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t off = e * PANEL + kk * 32;
+              mma_bf16_ss(tbase + lo + BC_SC, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_sc, kk > 0);
+              mma_bf16_ss(tbase + lo + BC_SC2, sdesc(da + off, 16, 1024), sdesc(va + off, 16, 1024), id_sc, kk > 0);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {  // scores and dP, K = 128 channels
+            const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
+            mma_bf16_ss(tbase + BC_SC, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_sc, kk > 0);
+            mma_bf16_ss(tbase + (16u << 16) + BC_SC, sdesc(da + off, 16, 1024), sdesc(va + off, 16, 1024), id_sc,
+                        kk > 0);
+          }
         }
         mma_commit(sc_full);
         ZTRACE(tr, 2, m);
@@ -214,37 +263,85 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         mbar_wait(sp_full, m & 1);
         tc_fence_after();
         ZTRACE(tr, 3, m);
+        if constexpr (PAIR) {
 #pragma unroll
-        for (int kk = 0; kk < T / 16; ++kk)  // dq^T = Kh^T dPm^T
-          mma_bf16_ss(tbase + BC_DQ, sdesc(ka + kk * 2048, PANEL, 1024), sdesc(dpma + kk * 32, 16, 1024), id_mk,
-                      kk > 0);
+          for (int e = 0; e < 2; ++e) {
+            const uint32_t lo = (16u * e) << 16;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)  // dq^T += S' dO^T
-          mma_bf16_ss(tbase + BC_DQ, sdesc(spa + (kk >> 2) * SPANEL + (kk & 3) * 32, 16, 1024),
-                      sdesc(da + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024), id_kk, 1);
-        mma_commit(sp_empty);
+            for (int kk = 0; kk < 4; ++kk)  // dq^T_e = Kh_e^T dPm_e^T
+              mma_bf16_ss(tbase + lo + BC_DQ, sdesc(ka + e * PANEL + kk * 2048, PANEL, 1024),
+                          sdesc(dpm_e[e] + kk * 32, 16, 1024), id_mk64, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < T / 16; ++kk) {  // dk^T = Qh^T dPm ; dv^T = dO^T Am  (independent of D')
-          mma_bf16_ss(tbase + BC_DK, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(dpma + kk * 2048, PANEL, 1024), id_mm,
-                      kk > 0);
-          mma_bf16_ss(tbase + BC_DV, sdesc(da + kk * 2048, PANEL, 1024), sdesc(ama + kk * 2048, PANEL, 1024), id_mm,
-                      kk > 0);
+            for (int kk = 0; kk < 4; ++kk)  // dq^T_e += S'_ee dO_e^T (rows 64e.. of panel e)
+              mma_bf16_ss(tbase + lo + BC_DQ, sdesc(spa + e * SPANEL + e * (T * 128) + kk * 32, 16, 1024),
+                          sdesc(da + e * PANEL + kk * 32, 16, 1024), id_kk64, 1);
+          }
+          mma_commit(sp_empty);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const uint32_t lo = (16u * e) << 16;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {  // dk^T_e = Qh_e^T dPm_e ; dv^T_e = dO_e^T Am_e
+              mma_bf16_ss(tbase + lo + BC_DK, sdesc(qa + e * PANEL + kk * 2048, PANEL, 1024),
+                          sdesc(dpm_e[e] + kk * 2048, PANEL, 1024), id_mm64, kk > 0);
+              mma_bf16_ss(tbase + lo + BC_DV, sdesc(da + e * PANEL + kk * 2048, PANEL, 1024),
+                          sdesc(am_e[e] + kk * 2048, PANEL, 1024), id_mm64, kk > 0);
+            }
+          }
+          mbar_wait(dp_ready, m & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const uint32_t lo = (16u * e) << 16;
+            const uint32_t dpe = dpa + e * SPANEL + e * (T * 128);  // D'_ee: rows 64e.. of panel e
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {  // dk^T_e += D'_ee V_e^T ; dv^T_e += D'_ee^T Kh_e^T
+              mma_bf16_ss(tbase + lo + BC_DK, sdesc(dpe + kk * 32, 16, 1024), sdesc(va + e * PANEL + kk * 32, 16, 1024),
+                          id_kk64, 1);
+              mma_bf16_ss(tbase + lo + BC_DV, sdesc(dpe + kk * 2048, SPANEL, 1024),
+                          sdesc(ka + e * PANEL + kk * 32, 16, 1024), id_mk64, 1);
+            }
+          }
+          mma_commit(grads_full);
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int kk = 0; kk < T / 16; ++kk)  // Dt_e += Qh_e^T dO_e
+              mma_bf16_ss(tbase + ((16u * e) << 16) + BC_QDO, sdesc(qa + e * PANEL + kk * 2048, PANEL, 1024),
+                          sdesc(da + e * PANEL + kk * 2048, PANEL, 1024), id_mm64, 1);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < T / 16; ++kk)  // dq^T = Kh^T dPm^T
+            mma_bf16_ss(tbase + BC_DQ, sdesc(ka + kk * 2048, PANEL, 1024), sdesc(dpma + kk * 32, 16, 1024), id_mk,
+                        kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)  // dq^T += S' dO^T
+            mma_bf16_ss(tbase + BC_DQ, sdesc(spa + (kk >> 2) * SPANEL + (kk & 3) * 32, 16, 1024),
+                        sdesc(da + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024), id_kk, 1);
+          mma_commit(sp_empty);
+#pragma unroll
+          for (int kk = 0; kk < T / 16; ++kk) {  // dk^T = Qh^T dPm ; dv^T = dO^T Am  (independent of D')
+            mma_bf16_ss(tbase + BC_DK, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(dpma + kk * 2048, PANEL, 1024), id_mm,
+                        kk > 0);
+            mma_bf16_ss(tbase + BC_DV, sdesc(da + kk * 2048, PANEL, 1024), sdesc(ama + kk * 2048, PANEL, 1024), id_mm,
+                        kk > 0);
+          }
+          mbar_wait(dp_ready, m & 1);  // D' in smem and Dt rescaled in TMEM
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {  // dk^T += D' V^T ; dv^T += D'^T Kh^T
+            const uint32_t boff = (kk >> 2) * PANEL + (kk & 3) * 32;
+            mma_bf16_ss(tbase + BC_DK, sdesc(dpa + (kk >> 2) * SPANEL + (kk & 3) * 32, 16, 1024),
+                        sdesc(va + boff, 16, 1024), id_kk, 1);
+            mma_bf16_ss(tbase + BC_DV, sdesc(dpa + kk * 2048, SPANEL, 1024), sdesc(ka + boff, 16, 1024), id_mk, 1);
+          }
+          mma_commit(grads_full);
+          // the state cotangent update is needed only by the next tile's rescale: issue it last
+#pragma unroll
+          for (int kk = 0; kk < T / 16; ++kk)  // Dt += Qh^T dO
+            mma_bf16_ss(tbase + BC_QDO, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(da + kk * 2048, PANEL, 1024),
+                        id_qdo, 1);
         }
-        mbar_wait(dp_ready, m & 1);  // D' in smem and Dt rescaled in TMEM
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {  // dk^T += D' V^T ; dv^T += D'^T Kh^T
-          const uint32_t boff = (kk >> 2) * PANEL + (kk & 3) * 32;
-          mma_bf16_ss(tbase + BC_DK, sdesc(dpa + (kk >> 2) * SPANEL + (kk & 3) * 32, 16, 1024),
-                      sdesc(va + boff, 16, 1024), id_kk, 1);
-          mma_bf16_ss(tbase + BC_DV, sdesc(dpa + kk * 2048, SPANEL, 1024), sdesc(ka + boff, 16, 1024), id_mk, 1);
-        }
-        mma_commit(grads_full);
-        // the state cotangent update is needed only by the next tile's rescale: issue it last
-#pragma unroll
-        for (int kk = 0; kk < T / 16; ++kk)  // Dt += Qh^T dO
-          mma_bf16_ss(tbase + BC_QDO, sdesc(qa + kk * 2048, PANEL, 1024), sdesc(da + kk * 2048, PANEL, 1024),
-                      id_qdo, 1);
         mma_commit(qdo_full);
         mma_commit(&empty[st]);  // QDO reads q / dO of this stage
         ZTRACE(tr, 4, m);
@@ -254,8 +351,8 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
     // ---------------- prep: one thread per channel c (warp w handles TMEM lane quarter w%4):
     //   logb over the 64 tile rows, r = logb[31], gamma = logb[63], Qh / Kh in place,
     //   d = logb - r -> TMEM (double buffered) for the epilogue
-    const int c = tid - 256;
-    const int quarter = c >> 5;
+    const int c = PAIR ? pair_channel(tid - 256) : tid - 256;  // PAIR: the channel of TMEM lane tid - 256
+    const int quarter = (tid - 256) >> 5;
     const uint32_t coff = (c >> 6) * PANEL + (c & 7) * 2, cchk = (c & 63) >> 3;
     constexpr float LOG2E = 1.4426950408889634f;
     for (int m = 0; m < nt; ++m) {
@@ -263,11 +360,12 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const int n = t1 - 1 - m;
       uint8_t* sb = smem + st * BO_STAGE;
       float lb[64];
-      const float* gp = g + hh * ghs + (long long)n * T * gts + c;
+      const float* gp = PAIR ? g + (2 * hh + (c >> 6)) * ghs + (long long)n * T * gts + (c & 63)
+                             : g + hh * ghs + (long long)n * T * gts + c;
       if constexpr (DENSE) {
 #pragma unroll
-        for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);  // immediate offsets
-      } else if (c < dr) {
+        for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * DW);  // immediate offsets
+      } else if (PAIR || c < dr) {
         const float* pr = gp;  // runtime stride: one pointer bump per row keeps the loads back to back
 #pragma unroll
         for (int r = 0; r < 64; ++r, pr += gts) lb[r] = __ldg(pr);
@@ -324,26 +422,33 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
     // ---------------- state / epilogue warps: thread (c, ch) owns Dt[c][64*ch .. +64] (TMEM) and,
     //                  in the epilogue, tokens [32*ch, 32*ch+32) of channel c
     const int qd = warp & 3, ch = warp >> 2;
-    const int c = 32 * qd + lane;
-    const uint32_t d_addr = taddr(tbase, 32 * qd, BC_QDO + 64 * ch);
+    // PAIR: this thread's TMEM lane holds channel c (head e = c / 64) and columns [32*ch, 32*ch+32) of that
+    // head's 64-column Dt block; otherwise channel 32*qd + lane and columns [64*ch, 64*ch+64)
+    const int c = PAIR ? pair_channel(32 * qd + lane) : 32 * qd + lane;
+    const int he = c >> 6;                                       // PAIR: head of the pair
+    const int vcol0 = PAIR ? 64 * he + 32 * ch : 64 * ch;        // first state column (v) of this thread
+    const uint32_t d_addr = taddr(tbase, 32 * qd, BC_QDO + (PAIR ? 32 * ch : 64 * ch));
+    constexpr int NHF = PAIR ? 1 : 2;                            // 32-column halves held per thread
     {
       const long long sidx = (long long)(hh * nseg + s) * D * D + c;  // column-major workspace states
       const float cgr = ds_next ? expf(cumGr[(hh * nseg + s) * D + c]) : 0.f;
       const float cg = s_prev ? expf(cumG[(hh * nseg + s) * D + c]) : 0.f;
       const float eg = expf(gamseg[(hh * nseg + s) * D + c]);
-      const long long pidx = ((long long)hh * dr + c) * dr + 64 * ch;  // API states are [h][dr][dr]
+      // API states are [h][dr][dr]; PAIR: head 2*hh + he, row c % 64
+      const long long pidx = PAIR ? ((long long)(2 * hh + he) * 64 + (c & 63)) * 64 + 32 * ch
+                                  : ((long long)hh * dr + c) * dr + 64 * ch;
       float rho = 0.f;
 #pragma unroll 1
-      for (int hf = 0; hf < 2; ++hf) {
+      for (int hf = 0; hf < NHF; ++hf) {
         float dv32[32];
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
           const int jj = 32 * hf + j;
-          const long long o = sidx + (long long)(64 * ch + jj) * D;
+          const long long o = sidx + (long long)(vcol0 + jj) * D;
           float4 dd = make_float4(Dend[o], Dend[o + D], Dend[o + 2 * D], Dend[o + 3 * D]);
           float4 si = make_float4(Sin[o], Sin[o + D], Sin[o + 2 * D], Sin[o + 3 * D]);
           const float4 ds = make_float4(dS[o], dS[o + D], dS[o + 2 * D], dS[o + 3 * D]);
-          const bool inb = c < dr && 64 * ch + jj < dr;
+          const bool inb = PAIR || (c < dr && 64 * ch + jj < dr);
           if (ds_next && inb) {
             const float4 a = *reinterpret_cast<const float4*>(ds_next + pidx + jj);
             dd.x = fmaf(cgr, a.x, dd.x); dd.y = fmaf(cgr, a.y, dd.y);
@@ -380,11 +485,13 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       mbar_wait(sc_full, m & 1);
       tc_fence_after();
       if (tid == 0) ZTRACE(tr, 5, m);
-      {
+#pragma unroll
+      for (int pass = 0; pass < (PAIR ? 2 : 1); ++pass) {  // PAIR: scores (lane half = head), then dP
         float a[32];
-        tmem_ld32(taddr(tbase, 32 * qd, BC_SC + 32 * ch), a);
+        tmem_ld32(taddr(tbase, 32 * qd, (PAIR && pass ? BC_SC2 : BC_SC) + 32 * ch), a);
         const int i = 16 * qd + (lane & 15);
-        uint8_t* dstbuf = lane < 16 ? am_buf : dpm_buf;
+        uint8_t* dstbuf = PAIR ? (pass ? (lane < 16 ? dpm_buf : dpm1_buf) : (lane < 16 ? am_buf : am1_buf))
+                               : (lane < 16 ? am_buf : dpm_buf);
 #pragma unroll
         for (int mm = 0; mm < 4; ++mm) {
           const int j0 = 32 * ch + 8 * mm;
@@ -410,9 +517,9 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       tc_fence_after();
       {
         const float f = fast_exp(gam_c - r_c + r_next);
-        uint8_t* dst = dp_buf + ch * SPANEL;
+        uint8_t* dst = dp_buf + (PAIR ? he : ch) * SPANEL;  // D' [c][v]: PAIR writes the head's diagonal block
 #pragma unroll 1
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int hf = 0; hf < NHF; ++hf) {
           float x[32];
           tmem_ld32_nw(d_addr + 32 * hf, *reinterpret_cast<uint32_t(*)[32]>(x));
           tmem_wait_ld();
@@ -426,7 +533,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
             w.y = pack_bf16(x[8 * mm + 2], x[8 * mm + 3]);
             w.z = pack_bf16(x[8 * mm + 4], x[8 * mm + 5]);
             w.w = pack_bf16(x[8 * mm + 6], x[8 * mm + 7]);
-            *reinterpret_cast<uint4*>(dst + sw128(c, 4 * hf + mm)) = w;
+            *reinterpret_cast<uint4*>(dst + sw128(c, (PAIR ? 4 * ch : 4 * hf) + mm)) = w;
           }
         }
       }
@@ -446,9 +553,10 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const long long tok0 = (long long)n * T + cols;  // token index inside the head
       float da[32];
       float tsum = 0.f;
-      __nv_bfloat16* pdq = dq + hh * gs.qh + tok0 * gs.qt + c;
-      __nv_bfloat16* pdk = dk + hh * gs.kh + tok0 * gs.kt + c;
-      __nv_bfloat16* pdv = dv + hh * gs.vh + tok0 * gs.vt + c;
+      const int oh = PAIR ? 2 * hh + he : hh, oc = PAIR ? (c & 63) : c;  // output head / channel
+      __nv_bfloat16* pdq = dq + oh * gs.qh + tok0 * gs.qt + oc;
+      __nv_bfloat16* pdk = dk + oh * gs.kh + tok0 * gs.kt + oc;
+      __nv_bfloat16* pdv = dv + oh * gs.vh + tok0 * gs.vt + oc;
 #pragma unroll
       for (int h8 = 0; h8 < 4; ++h8) {
         uint32_t gq[8], gk[8], gv8[8], dl[8];
@@ -473,7 +581,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           const float dlt = __uint_as_float(dl[u]);  // (logb - r) * log2(e), from the prep warps
           da[i] = __fsub_rn(__fmul_rn(qh[u], q_raw), __fmul_rn(kh[u], k_raw));  // no FMA contraction: identical in every variant
           tsum += da[i];
-          if (DENSE || c < dr) {  // channels of a d = 64 head beyond 64 are padding
+          if (DENSE || PAIR || c < dr) {  // channels of a d = 64 head beyond 64 are padding
             *pdq = __float2bfloat16_rn(q_raw * fast_exp2(dlt));
             *pdk = __float2bfloat16_rn(k_raw * fast_exp2(-dlt));
             *pdv = __float2bfloat16_rn(__uint_as_float(gv8[u]));
@@ -490,10 +598,10 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const float rho_end = xr[c];
       const float t_upper = xcarry[D + c], t_lower = xcarry[c];
       float base = rho_end + (ch == 0 ? t_lower + t_upper : t_upper);
-      float* pdg = dg + hh * gs.gh + tok0 * gs.gt + c;
+      float* pdg = dg + oh * gs.gh + tok0 * gs.gt + oc;
 #pragma unroll
       for (int i = 0; i < 32; ++i, pdg += gs.gt) {
-        if (DENSE || c < dr) *pdg = base;
+        if (DENSE || PAIR || c < dr) *pdg = base;
         base -= da[i];
       }
       if (tid == 0) ZTRACE(tr, 9, m);
@@ -518,6 +626,29 @@ int fast_bwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
   CUtensorMap mq, mk, mv, mdo, msp, mg;
+  const int early = pdl_enabled() && early_inputs();
+  if (pl.pair) {
+    const int heads = 2 * pl.h;
+    if (int rc = map_act_pair(&mq, q, pl.L, heads)) return rc;
+    if (int rc = map_act_pair(&mk, k, pl.L, heads)) return rc;
+    if (int rc = map_act_pair(&mv, v, pl.L, heads)) return rc;
+    if (int rc = map_act_pair(&mdo, d_out, pl.L, heads)) return rc;
+    if (int rc = sp_map_pair(&msp, w.Sp, pl)) return rc;
+    if (int rc = map_gate_pair(&mg, g, pl.L, heads)) return rc;
+    const Strides4 gs{(int)dq.ts, (int)dk.ts, (int)dv.ts, (int)dg.ts, dq.hs, dk.hs, dv.hs, dg.hs};
+    const bool dn = is_dense64(g, pl.L) && is_dense64(dq, pl.L) && is_dense64(dk, pl.L) && is_dense64(dv, pl.L) &&
+                    is_dense64(dg, pl.L);
+    auto kern = dn ? bwd_out_kernel<true, true> : bwd_out_kernel<false, true>;
+    set_smem_once((const void*)kern, (int)BO_SMEM);
+    if (cudaError_t e = launch_kp(pdl_enabled(), kern, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp,
+                                  mg, (const float*)g.p, g.ts, g.hs, pl.L, 1, 64, pl.nseg, pl.ntiles,
+                                  (const float*)w.Sin, (const float*)w.cumG, (const float*)w.dS, (const float*)w.gam,
+                                  (const float*)s_prev, (const float*)w.Dend, (const float*)w.cumGr,
+                                  (const float*)ds_next, (__nv_bfloat16*)dq.p, (__nv_bfloat16*)dk.p,
+                                  (__nv_bfloat16*)dv.p, (float*)dg.p, gs, g_trace_buf, g_trace_cta, early))
+      return cuda_fail(e, "bwd_out_kernel (pairs)");
+    return zgla_check_launch();
+  }
   const bool din = is_dense(q, pl.L) && is_dense(k, pl.L) && is_dense(v, pl.L) && is_dense(d_out, pl.L);
   const bool dn = is_dense(g, pl.L) && is_dense(dq, pl.L) && is_dense(dk, pl.L) && is_dense(dv, pl.L) &&
                   is_dense(dg, pl.L);
@@ -530,7 +661,6 @@ int fast_bwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   const Strides4 gs{(int)dq.ts, (int)dk.ts, (int)dv.ts, (int)dg.ts, dq.hs, dk.hs, dv.hs, dg.hs};
   auto kern = dn ? bwd_out_kernel<true> : bwd_out_kernel<false>;
   set_smem_once((const void*)kern, (int)BO_SMEM);
-  const int early = pdl_enabled() && early_inputs();
   if (cudaError_t e = launch_kp(pdl_enabled(), kern, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp, mg,
                                 (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
                                 (const float*)w.Sin, (const float*)w.cumG, (const float*)w.dS, (const float*)w.gam, (const float*)s_prev,

@@ -45,8 +45,9 @@ constexpr int SPANEL = D * 128;        // one 64-column panel of a [D x D] bf16 
 constexpr int STATE_BF16 = D * D * 2;  // 32 KiB
 
 struct Plan {
-  int h, nseg, ntiles;
+  int h, nseg, ntiles;  // h: CTA heads (head PAIRS when pair != 0)
   long long L;
+  int pair;  // d = 64 with an even head count: two heads per 128-channel CTA
 };
 
 __host__ __device__ inline void seg_range(int s, int nseg, int ntiles, int& t0, int& t1) {
@@ -100,12 +101,18 @@ inline Ws carve(const Plan& p, void* base) {
   return w;
 }
 
+inline bool pair_mode(const zgla_shape* s) {
+  static const bool off = std::getenv("ZGLA_NO_PAIR") != nullptr;  // A/B: d = 64 heads zero-filled to 128
+  return s->key_dim == 64 && s->heads % 2 == 0 && !off;
+}
+
 inline Plan make_plan(const zgla_shape* s, int num_sms) {
   Plan p;
-  p.h = s->heads;
+  p.pair = pair_mode(s) ? 1 : 0;
+  p.h = p.pair ? s->heads / 2 : s->heads;
   p.L = s->seq_len;
   p.ntiles = (int)(s->seq_len / T);
-  int nseg = num_sms / (s->heads > 0 ? s->heads : 1);
+  int nseg = num_sms / (p.h > 0 ? p.h : 1);
   if (nseg < 1) nseg = 1;
   if (nseg > p.ntiles) nseg = p.ntiles;
   p.nseg = nseg;
@@ -208,9 +215,20 @@ inline int sp_map(CUtensorMap* m, void* sp, const Plan& pl, int dr) {
   return make_map(m, sp, true, (unsigned long long)pl.h * pl.ntiles * 64, 64, 64, 64, true);
 }
 inline bool is_dense(const TRef& r, long long L) { return r.dr == D && r.ts == D && r.hs == L * D; }
+inline bool is_dense64(const TRef& r, long long L) { return r.dr == 64 && r.ts == 64 && r.hs == L * 64; }
 inline int map_act(CUtensorMap* m, const TRef& r, long long L, int heads, bool dense) {  // bf16 64x64 SW128
   if (dense) return make_map(m, r.p, true, (unsigned long long)heads * L, D, 64, T, true);
   return make_map3(m, r, true, L, heads, 64, T, true);
+}
+// PAIR: per-head 64 x 64 boxes over (channels, tokens, heads) maps
+inline int map_act_pair(CUtensorMap* m, const TRef& r, long long L, int heads) {
+  return make_map3(m, r, true, L, heads, 64, T, true);
+}
+inline int map_gate_pair(CUtensorMap* m, const TRef& r, long long L, int heads) {
+  return make_map3(m, r, false, L, heads, 64, T, false);
+}
+inline int sp_map_pair(CUtensorMap* m, void* sp, const Plan& pl) {  // [2 h NT 64 rows][64], per-head blocks
+  return make_map(m, sp, true, (unsigned long long)2 * pl.h * pl.ntiles * 64, 64, 64, 64, true);
 }
 inline int map_gate(CUtensorMap* m, const TRef& r, long long L, int heads, bool dense) {  // fp32 128x64 boxes
   if (dense) return make_map(m, r.p, false, (unsigned long long)heads * L, D, D, T, false);

@@ -31,7 +31,9 @@ constexpr int KS_THREADS = 320;                     // 8 prep warps (2 groups), 
 constexpr int KS_OFF_BAR = KS_NS * KS_STAGE;
 constexpr size_t KS_SMEM = 1024 + KS_NS * KS_STAGE + 4096;
 
-template <int DIR, bool DENSE>  // 0: forward local state (a=k, b=v, reverse walk); 1: backward (a=q, b=dO)
+// PAIR (d = 64): the CTA's 128 channels are two heads, 2*hh (channels 0-63) and 2*hh+1 (64-127); the state
+// accumulator keeps its cross-head blocks, which no consumer reads (see fwd_out_kernel)
+template <int DIR, bool DENSE, bool PAIR = false>  // 0: forward local state (a=k, b=v, reverse walk); 1: backward (a=q, b=dO)
 __global__ void __launch_bounds__(KS_THREADS, 1)
     seg_state_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                      const __grid_constant__ CUtensorMap tm_g, long long L, int in3d, int nseg, int ntiles,
@@ -95,11 +97,20 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], KS_STAGE);
         const int r = tile * T;
-        tile_load<DENSE>(sa, &tm_a, &full[st], 0, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sa + PANEL, &tm_a, &full[st], 64, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sa + TILE_BF16, &tm_b, &full[st], 0, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sa + TILE_BF16 + PANEL, &tm_b, &full[st], 64, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sa + 2 * TILE_BF16, &tm_g, &full[st], 0, r, hh, L, in3d, pol);
+        if constexpr (PAIR) {  // one 64-channel panel per head; gates as two [64][64] fp32 blocks
+          tile_load<false>(sa, &tm_a, &full[st], 0, r, 2 * hh, L, 1, pol);
+          tile_load<false>(sa + PANEL, &tm_a, &full[st], 0, r, 2 * hh + 1, L, 1, pol);
+          tile_load<false>(sa + TILE_BF16, &tm_b, &full[st], 0, r, 2 * hh, L, 1, pol);
+          tile_load<false>(sa + TILE_BF16 + PANEL, &tm_b, &full[st], 0, r, 2 * hh + 1, L, 1, pol);
+          tile_load<false>(sa + 2 * TILE_BF16, &tm_g, &full[st], 0, r, 2 * hh, L, 1, pol);
+          tile_load<false>(sa + 2 * TILE_BF16 + TILE_F32 / 2, &tm_g, &full[st], 0, r, 2 * hh + 1, L, 1, pol);
+        } else {
+          tile_load<DENSE>(sa, &tm_a, &full[st], 0, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sa + PANEL, &tm_a, &full[st], 64, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sa + TILE_BF16, &tm_b, &full[st], 0, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sa + TILE_BF16 + PANEL, &tm_b, &full[st], 64, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sa + 2 * TILE_BF16, &tm_g, &full[st], 0, r, hh, L, in3d, pol);
+        }
       }
     }
   } else if (warp == 9) {
@@ -135,8 +146,14 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
       const float* gs = reinterpret_cast<const float*>(sa + 2 * TILE_BF16);
       mbar_wait(&full[st], ph);
       float lb[64];
+      if constexpr (PAIR) {
+        const float* gh = gs + (c >> 6) * (T * 64) + (c & 63);
 #pragma unroll
-      for (int r = 0; r < 64; ++r) lb[r] = gs[r * D + c];
+        for (int r = 0; r < 64; ++r) lb[r] = gh[r * 64];
+      } else {
+#pragma unroll
+        for (int r = 0; r < 64; ++r) lb[r] = gs[r * D + c];
+      }
       if (DIR == 0) {  // the reference's SeqShard check (glasp/gla.py:106-107): every gate finite and < 0
         float mx = lb[0];
 #pragma unroll
@@ -215,10 +232,12 @@ __device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
 }
 // DIR 0 (K2): Sin / cumG / S_local / G_tot;  DIR 1 (K5): Dend / cumGr / ds_local0 (segments walked
 // from the last).  Four adjacent channels per thread: 16-byte loads and stores.
+// pair != 0: d = 64 head pairs; the API outputs take the two diagonal 64 x 64 blocks (heads 2*hh, 2*hh+1)
 template <int DIR>
 __global__ void seg_scan_kernel(int h, int nseg, int dr, const float* __restrict__ dS, const float* __restrict__ gam,
                                 float* __restrict__ Sin, float* __restrict__ cumG, float* __restrict__ s_local,
-                                float* __restrict__ g_tot, const float* __restrict__ pf0, const float* __restrict__ pf1) {
+                                float* __restrict__ g_tot, const float* __restrict__ pf0, const float* __restrict__ pf1,
+                                int pair) {
   pdl_wait();
   pdl_trigger();
   const long long idx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
@@ -253,6 +272,16 @@ __global__ void seg_scan_kernel(int h, int nseg, int dr, const float* __restrict
     }
   }
   const float rv[4] = {run.x, run.y, run.z, run.w}, cv[4] = {cm.x, cm.y, cm.z, cm.w};
+  if (pair) {  // four channels of one head (c % 4 == 0 never straddles the 64-channel halves)
+    const int e = c >> 6, head = 2 * hh + e;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int cc = (c & 63) + u;
+      if (s_local && (vv >> 6) == e) s_local[((long long)head * 64 + cc) * 64 + (vv & 63)] = rv[u];
+      if (DIR == 0 && vv == 0 && g_tot) g_tot[head * 64 + cc] = cv[u];
+    }
+    return;
+  }
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     if (s_local && c + u < dr && vv < dr) s_local[((long long)hh * dr + c + u) * dr + vv] = rv[u];
@@ -274,7 +303,11 @@ constexpr size_t FO_SMEM = 1024 + FO_OFF_BAR + 256;
 // TMEM columns
 constexpr uint32_t COL_KV = 0, COL_O = 128, COL_A = 256, COL_S = 320;
 
-template <bool DENSE>
+// PAIR (d = 64, heads 2*hh and 2*hh+1 on channels 0-63 / 64-127): the scores, the intra term and the
+// inter term are per head (K = 64 halves into separate accumulators / output column halves); the fp32
+// state keeps its cross-head blocks, which only the (cheap, full-width) state MMA writes and nobody reads.
+// The second masked-score operand lives in the off-diagonal (unused) half of the S' buffer.
+template <bool DENSE, bool PAIR = false>
 __global__ void __launch_bounds__(FO_THREADS, 1)
     fwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g,
@@ -313,11 +346,13 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
   const int nt = t1 - t0;
   unsigned long long* tr = (trace != nullptr && (int)blockIdx.x == trace_cta) ? trace : nullptr;
   if (trace != nullptr && threadIdx.x == 0) cta_trace_begin(trace);
+  constexpr int DW = PAIR ? 64 : D;  // channels per head in memory
   if constexpr (DENSE) {  // compile-time strides for the dense layout
-    gts = D, ots = D;
-    ghs = L * D, ohs = L * D;
-    dr = D;
+    gts = DW, ots = DW;
+    ghs = L * DW, ohs = L * DW;
+    dr = DW;
   }
+  uint8_t* am1_buf = sp_buf + T * 128;  // PAIR: rows 64-127 of S' panel 0 (the cross-head block)
 
   if (tid == 0) {
     for (int i = 0; i < FO_NS; ++i) {
@@ -362,18 +397,33 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], FO_STAGE);
         const int r = (t0 + n) * T;
-        tile_load<DENSE>(sb, &tm_q, &full[st], 0, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + PANEL, &tm_q, &full[st], 64, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + TILE_BF16, &tm_k, &full[st], 0, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r, hh, L, in3d, pol);
-        tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d, pol);
+        if constexpr (PAIR) {
+#pragma unroll
+          for (int x = 0; x < 3; ++x) {
+            const CUtensorMap* mx = x == 0 ? &tm_q : x == 1 ? &tm_k : &tm_v;
+            tile_load<false>(sb + x * TILE_BF16, mx, &full[st], 0, r, 2 * hh, L, 1, pol);
+            tile_load<false>(sb + x * TILE_BF16 + PANEL, mx, &full[st], 0, r, 2 * hh + 1, L, 1, pol);
+          }
+        } else {
+          tile_load<DENSE>(sb, &tm_q, &full[st], 0, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + PANEL, &tm_q, &full[st], 64, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + TILE_BF16, &tm_k, &full[st], 0, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + TILE_BF16 + PANEL, &tm_k, &full[st], 64, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + 2 * TILE_BF16, &tm_v, &full[st], 0, r, hh, L, in3d, pol);
+          tile_load<DENSE>(sb + 2 * TILE_BF16 + PANEL, &tm_v, &full[st], 64, r, hh, L, in3d, pol);
+        }
 #if ZGLA_G_PREFETCH_FWD
         // warm L2 with the gate tile the prep warps read (pointer loads) a few tiles from now
         if (n + ZGLA_G_PREFETCH_FWD < nt) {
           const int rg = (t0 + n + ZGLA_G_PREFETCH_FWD) * T;
-          if (in3d) tma_prefetch_3d(&tm_g, 0, rg, hh);
-          else tma_prefetch_2d(&tm_g, 0, (int)(hh * L + rg));
+          if constexpr (PAIR) {
+            tma_prefetch_3d(&tm_g, 0, rg, 2 * hh);
+            tma_prefetch_3d(&tm_g, 0, rg, 2 * hh + 1);
+          } else if (in3d) {
+            tma_prefetch_3d(&tm_g, 0, rg, hh);
+          } else {
+            tma_prefetch_2d(&tm_g, 0, (int)(hh * L + rg));
+          }
         }
 #endif
         ZTRACE(tr, 0, n);
@@ -386,7 +436,8 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       constexpr uint32_t id_qs = idesc_bf16(64, 128, false, true);
       constexpr uint32_t id_kv = idesc_bf16(128, 128, true, true);
       constexpr uint32_t id_av = idesc_bf16(64, 128, false, true);
-      const uint32_t spa = smem_u32(sp_buf), ama = smem_u32(am_buf);
+      constexpr uint32_t id_h64 = idesc_bf16(64, 64, false, true);  // PAIR: per-head inter / intra (N = 64)
+      const uint32_t spa = smem_u32(sp_buf), ama = smem_u32(am_buf), am1a = smem_u32(am1_buf);
       const bool save_sp = sp_save != nullptr;
       if (save_sp) tma_prefetch_desc(&tm_sp);
       for (int n = 0; n < nt; ++n) {
@@ -399,13 +450,20 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
-          mma_bf16_ss(tbase + COL_A, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_sc, kk > 0);
+          if constexpr (PAIR)  // per-head scores: head 1's in the other lane half of the same columns
+            mma_bf16_ss(tbase + ((kk >> 2) ? (16u << 16) : 0u) + COL_A, sdesc(qa + off, 16, 1024),
+                        sdesc(ka + off, 16, 1024), id_sc, (kk & 3) > 0);
+          else
+            mma_bf16_ss(tbase + COL_A, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_sc, kk > 0);
         }
         mma_commit(a_full);
         ZTRACE(tr, 2, n);
         mbar_wait(s_ready, n & 1);
         if (save_sp) {  // chunk-start state for the backward: async bulk store straight from smem
-          if (dr == D) {
+          if constexpr (PAIR) {  // the two diagonal 64 x 64 blocks, stored per head
+            tma_store_2d(&tm_sp, sp_buf, 0, ((2 * hh) * ntiles + t0 + n) * 64);
+            tma_store_2d(&tm_sp, sp_buf + SPANEL + T * 128, 0, ((2 * hh + 1) * ntiles + t0 + n) * 64);
+          } else if (dr == D) {
             const int rs = (hh * ntiles + t0 + n) * D;
             tma_store_2d(&tm_sp, sp_buf, 0, rs);
             tma_store_2d(&tm_sp, sp_buf + SPANEL, 64, rs);
@@ -422,7 +480,11 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
-          mma_bf16_ss(t_o, sdesc(qa + off, 16, 1024), sdesc(spa + kk * 2048, SPANEL, 1024), id_qs, kk > 0);
+          if constexpr (PAIR)  // O[:, 64e:64e+64] = Qh_e S'_ee (K = the head's 64 channels)
+            mma_bf16_ss(t_o + 64 * (kk >> 2), sdesc(qa + off, 16, 1024),
+                        sdesc(spa + (kk >> 2) * SPANEL + kk * 2048, SPANEL, 1024), id_h64, (kk & 3) > 0);
+          else
+            mma_bf16_ss(t_o, sdesc(qa + off, 16, 1024), sdesc(spa + kk * 2048, SPANEL, 1024), id_qs, kk > 0);
         }
         mbar_wait(kv_empty, (n & 1) ^ 1);
         tc_fence_after();
@@ -436,8 +498,15 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         mbar_wait(a_done, n & 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < T / 16; ++kk)
-          mma_bf16_ss(t_o, sdesc(ama + kk * 32, 16, 1024), sdesc(va + kk * 2048, PANEL, 1024), id_av, 1);
+        for (int kk = 0; kk < T / 16; ++kk) {
+          if constexpr (PAIR) {  // O[:, 64e:64e+64] += mask(A_e) V_e
+            mma_bf16_ss(t_o, sdesc(ama + kk * 32, 16, 1024), sdesc(va + kk * 2048, PANEL, 1024), id_h64, 1);
+            mma_bf16_ss(t_o + 64, sdesc(am1a + kk * 32, 16, 1024), sdesc(va + PANEL + kk * 2048, PANEL, 1024),
+                        id_h64, 1);
+          } else {
+            mma_bf16_ss(t_o, sdesc(ama + kk * 32, 16, 1024), sdesc(va + kk * 2048, PANEL, 1024), id_av, 1);
+          }
+        }
         mma_commit(o_full);
         mma_commit(&empty[st]);
         ZTRACE(tr, 4, n);
@@ -455,11 +524,12 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       const int st = n % FO_NS, ph = (n / FO_NS) & 1;
       uint8_t* sb = smem + st * FO_STAGE;
       float lb[64];
-      const float* gp = g + hh * ghs + (long long)(t0 + n) * T * gts + c;
+      const float* gp = PAIR ? g + (2 * hh + (c >> 6)) * ghs + (long long)(t0 + n) * T * gts + (c & 63)
+                             : g + hh * ghs + (long long)(t0 + n) * T * gts + c;
       if constexpr (DENSE) {
 #pragma unroll
-        for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * D);  // immediate offsets
-      } else if (c < dr) {
+        for (int r = 0; r < 64; ++r) lb[r] = __ldg(gp + r * DW);  // immediate offsets
+      } else if (PAIR || c < dr) {
         const float* pr = gp;  // runtime stride: one pointer bump per row keeps the loads back to back
 #pragma unroll
         for (int r = 0; r < 64; ++r, pr += gts) lb[r] = __ldg(pr);
@@ -507,6 +577,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
     const uint32_t s_addr = taddr(tbase, 32 * qd, COL_S);
     // S' = scale * S for 32 columns [32*q, 32*q+32) -> smem B operand ([dk rows][dv], 2 SW128 panels)
     auto write_sp = [&](const float (&v)[32], int q, float scale) {
+      if (PAIR && (q >> 1) != (c >> 6)) return;  // PAIR: only the head's diagonal block (the other is A_1)
       uint8_t* dst = sp_buf + (q >> 1) * SPANEL;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
@@ -521,7 +592,10 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
     {
       const long long sidx = (long long)(hh * nseg + s) * D * D + c;  // column-major workspace state
       const float cg = s_prev ? expf(cumG[(hh * nseg + s) * D + c]) : 0.f;
-      const float* pv = (s_prev && c < dr) ? s_prev + ((long long)hh * dr + c) * dr : nullptr;
+      // API states are [head][dr][dr]; PAIR: row c of head 2*hh + c/64, applied to that head's 64 columns
+      const float* pv = !s_prev ? nullptr
+                        : PAIR ? s_prev + ((long long)(2 * hh + (c >> 6)) * 64 + (c & 63)) * 64 - 64 * (c >> 6)
+                        : c < dr ? s_prev + ((long long)hh * dr + c) * dr : nullptr;
       // all loads first (two batches of 64 values, straight into TMEM); the bf16 copy S' needs the first
       // tile's reference point, so it is written from TMEM once the prep warps have published it
 #pragma unroll 1
@@ -534,7 +608,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
             const int col = 32 * (q2 + hq) + j;
             float4 a = make_float4(Sin[sidx + col * D], Sin[sidx + (col + 1) * D], Sin[sidx + (col + 2) * D],
                                    Sin[sidx + (col + 3) * D]);
-            if (pv && col < dr) {
+            if (pv && (PAIR ? (col >> 6) == (c >> 6) : col < dr)) {
               const float4 b = *reinterpret_cast<const float4*>(pv + col);
               a.x += cg * b.x;
               a.y += cg * b.y;
@@ -574,8 +648,9 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
       for (int hf = 0; hf < 2; ++hf) {
         float a[32];
         tmem_ld32(taddr(tbase, 32 * qd, COL_A + 32 * hf), a);
-        if (lane < 16) {
-          const int i = 16 * qd + lane;
+        if (PAIR || lane < 16) {  // PAIR: lanes 16-31 hold head 1's scores
+          const int i = 16 * qd + (lane & 15);
+          uint8_t* amb = (PAIR && lane >= 16) ? am1_buf : am_buf;
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
             uint4 w;
@@ -584,7 +659,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
             w.y = pack_bf16(j0 + 2 <= i ? a[8 * m + 2] : 0.f, j0 + 3 <= i ? a[8 * m + 3] : 0.f);
             w.z = pack_bf16(j0 + 4 <= i ? a[8 * m + 4] : 0.f, j0 + 5 <= i ? a[8 * m + 5] : 0.f);
             w.w = pack_bf16(j0 + 6 <= i ? a[8 * m + 6] : 0.f, j0 + 7 <= i ? a[8 * m + 7] : 0.f);
-            *reinterpret_cast<uint4*>(am_buf + sw128(i, 4 * hf + m)) = w;
+            *reinterpret_cast<uint4*>(amb + sw128(i, 4 * hf + m)) = w;
           }
         }
       }
@@ -637,7 +712,7 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         named_bar(3, 128);
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {
-          if (32 * q >= dr) break;
+          if (!PAIR && 32 * q >= dr) break;
           float o[32];
           tmem_ld32(taddr(tbase, 32 * qd, COL_O + 32 * q), o);
           if ((lane >> 4) == ob) {
@@ -659,9 +734,14 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         fence_proxy_async();
         named_bar(3, 128);
         if (tid == 0) {
-          const int row = (int)(hh * L + (long long)(t0 + n) * T);
-          tma_store_2d(&tm_o, os, 0, row);
-          if (dr == D) tma_store_2d(&tm_o, os + PANEL, 64, row);
+          if constexpr (PAIR) {  // staging panel e -> head 2*hh + e ([h * L rows][64] map)
+            tma_store_2d(&tm_o, os, 0, (int)(2 * hh * L + (long long)(t0 + n) * T));
+            tma_store_2d(&tm_o, os + PANEL, 0, (int)((2 * hh + 1) * L + (long long)(t0 + n) * T));
+          } else {
+            const int row = (int)(hh * L + (long long)(t0 + n) * T);
+            tma_store_2d(&tm_o, os, 0, row);
+            if (dr == D) tma_store_2d(&tm_o, os + PANEL, 64, row);
+          }
           tma_store_commit();
         }
       } else {  // strided / d = 64 outputs: 16-byte row pieces straight from the lane half that holds them
@@ -669,9 +749,11 @@ __global__ void __launch_bounds__(FO_THREADS, 1)
         for (int q = 0; q < 4; ++q) {
           float o[32];
           tmem_ld32(taddr(tbase, 32 * qd, COL_O + 32 * q), o);
-          if ((lane >> 4) == ob && 32 * q < dr) {
+          if ((lane >> 4) == ob && (PAIR || 32 * q < dr)) {
             const int i = 16 * qd + (lane & 15);
-            uint4* dst = reinterpret_cast<uint4*>(out + hh * ohs + ((long long)(t0 + n) * T + i) * ots + 32 * q);
+            uint4* dst = reinterpret_cast<uint4*>(
+                PAIR ? out + (2 * hh + (q >> 1)) * ohs + ((long long)(t0 + n) * T + i) * ots + 32 * (q & 1)
+                     : out + hh * ohs + ((long long)(t0 + n) * T + i) * ots + 32 * q);
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
               uint4 w;
@@ -713,6 +795,18 @@ int* domain_sink_of(const void* ws);
 int launch_seg_state(int dir, const Plan& pl, const TRef& a, const TRef& b, const TRef& g, float* out_state,
                      float* out_gam, int* flags, cudaStream_t st, int* dom_sink = nullptr) {
   CUtensorMap ma, mb, mg;
+  if (pl.pair) {
+    const int heads = 2 * pl.h;
+    if (int rc = map_act_pair(&ma, a, pl.L, heads)) return rc;
+    if (int rc = map_act_pair(&mb, b, pl.L, heads)) return rc;
+    if (int rc = map_gate_pair(&mg, g, pl.L, heads)) return rc;
+    auto kern = dir == 0 ? seg_state_kernel<0, false, true> : seg_state_kernel<1, false, true>;
+    set_smem_once((const void*)kern, (int)KS_SMEM);
+    if (cudaError_t e = launch_k(kern, pl.h * pl.nseg, KS_THREADS, KS_SMEM, st, ma, mb, mg, pl.L, 1, pl.nseg,
+                                  pl.ntiles, out_state, out_gam, flags, dom_sink))
+      return cuda_fail(e, "seg_state_kernel (pairs)");
+    return zgla_check_launch();
+  }
   const bool dn = is_dense(a, pl.L) && is_dense(b, pl.L) && is_dense(g, pl.L);  // all TMA-read
   if (int rc = map_act(&ma, a, pl.L, pl.h, dn)) return rc;
   if (int rc = map_act(&mb, b, pl.L, pl.h, dn)) return rc;
@@ -733,7 +827,7 @@ int fast_fwd_local(const zgla_shape* s, int num_sms, const TRef& k, const TRef& 
   const long long n = (long long)pl.h * D * D;
   if (cudaError_t e = launch_k(seg_scan_kernel<0>, (unsigned)((n / 4 + 127) / 128), 128, 0, st, pl.h, pl.nseg, k.dr,
                                 (const float*)w.dS, (const float*)w.gam, w.Sin, w.cumG, (float*)s_local, (float*)g_tot,
-                                (const float*)nullptr, (const float*)nullptr))
+                                (const float*)nullptr, (const float*)nullptr, pl.pair))
     return cuda_fail(e, "seg_scan_kernel<0>");
   return zgla_check_launch();
 }
@@ -743,6 +837,27 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
   CUtensorMap mq, mk, mv, mg, msp;
+  const int early = pdl_enabled() && early_inputs();
+  if (pl.pair) {
+    const int heads = 2 * pl.h;
+    if (int rc = sp_map_pair(&msp, w.Sp, pl)) return rc;
+    if (int rc = map_act_pair(&mq, q, pl.L, heads)) return rc;
+    if (int rc = map_act_pair(&mk, k, pl.L, heads)) return rc;
+    if (int rc = map_act_pair(&mv, v, pl.L, heads)) return rc;
+    if (int rc = map_gate_pair(&mg, g, pl.L, heads)) return rc;
+    const bool dn = is_dense64(g, pl.L) && is_dense64(o, pl.L) && ZGLA_O_TMA;
+    CUtensorMap mo = mq;
+    if (dn)
+      if (int rc = make_map(&mo, o.p, true, (unsigned long long)heads * pl.L, 64, 64, T, true)) return rc;
+    auto kern = dn ? fwd_out_kernel<true, true> : fwd_out_kernel<false, true>;
+    set_smem_once((const void*)kern, (int)FO_SMEM);
+    if (cudaError_t e = launch_kp(pdl_enabled(), kern, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
+                                  mo, (const float*)g.p, g.ts, g.hs, pl.L, 1, 64, pl.nseg, pl.ntiles,
+                                  (const float*)w.Sin, (const float*)w.cumG, (const float*)s_prev, (__nv_bfloat16*)o.p,
+                                  o.ts, o.hs, w.Sp, g_trace_buf, g_trace_cta, early))
+      return cuda_fail(e, "fwd_out_kernel (pairs)");
+    return zgla_check_launch();
+  }
   // maps: 2-D iff the TMA-read inputs are dense; kernel variant: compile-time strides iff the
   // pointer-addressed tensors (g, o) are dense
   const bool din = is_dense(q, pl.L) && is_dense(k, pl.L) && is_dense(v, pl.L);
@@ -757,7 +872,6 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
     if (int rc = map_act(&mo, o, pl.L, pl.h, true)) return rc;
   auto kern = dn ? fwd_out_kernel<true> : fwd_out_kernel<false>;
   set_smem_once((const void*)kern, (int)FO_SMEM);
-  const int early = pdl_enabled() && early_inputs();
   if (cudaError_t e = launch_kp(pdl_enabled(), kern, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
                                 mo, (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
                                 (const float*)w.Sin, (const float*)w.cumG, (const float*)s_prev, (__nv_bfloat16*)o.p,
@@ -775,7 +889,7 @@ int fast_bwd_local(const zgla_shape* s, int num_sms, const TRef& q, const TRef& 
   const long long n = (long long)pl.h * D * D;
   if (cudaError_t e = launch_k(seg_scan_kernel<1>, (unsigned)((n / 4 + 127) / 128), 128, 0, st, pl.h, pl.nseg, q.dr,
                                 (const float*)w.dD, (const float*)w.gam, w.Dend, w.cumGr, (float*)ds0, (float*)nullptr,
-                                (const float*)w.Sin, (const float*)w.dS))
+                                (const float*)w.Sin, (const float*)w.dS, pl.pair))
     return cuda_fail(e, "seg_scan_kernel<1>");
   return zgla_check_launch();
 }
