@@ -215,6 +215,8 @@ int zgla_selftest_stream(const void* src, long long rows, int tiles_per_cta, int
                          int ctas, void* stream);
 int zgla_selftest_mma(const void* a, const void* b, float* d, int M, int N, int K, int a_mn, int b_mn,
                       int lane_off, void* stream);
+/* diagnostics: one CTA spinning for ns nanoseconds on the stream (injected-latency probes) */
+int zgla_selftest_spin(long long ns, void* stream);
 
 #ifdef __cplusplus
 }

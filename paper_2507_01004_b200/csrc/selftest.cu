@@ -231,3 +231,18 @@ extern "C" int zgla_selftest_tmem(int nwarps, int iters, int mode, long long* ou
   selftest_tmem_kernel<<<1, 32 * nwarps, 0, (cudaStream_t)stream>>>(iters, mode, out, sink);
   return zgla_check_launch();
 }
+
+// ---- injected latency (diagnostics): one 32-thread CTA that spins on %globaltimer for `ns` nanoseconds.
+// scripts/overlap_probe.py puts it where a peer's All-Scan chain would sit on one GPU, to measure how much
+// of a chain's latency the head-group overlap schedule (ZecoRank overlap_groups) hides.
+__global__ void __launch_bounds__(32) selftest_spin_kernel(long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  } while ((long long)(t - t0) < ns);
+}
+extern "C" int zgla_selftest_spin(long long ns, void* stream) {
+  selftest_spin_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ns);
+  return zgla_check_launch();
+}

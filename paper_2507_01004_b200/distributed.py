@@ -68,6 +68,11 @@ class AllScanP2P:
                      ops._p(scanned), ops._stream())
         return recv, scanned
 
+    def split(self, heads):
+        """A communicator over the same ranks for ``heads`` heads (one per head group of ZecoRank's
+        overlap schedule; each group's chain has its own inboxes and epochs)."""
+        return AllScanP2P(heads, self.shape[1], self.shape[2], group=self.group)
+
     def check(self, sync: bool = True) -> None:
         """DeadlockError if a chain wait of an earlier call timed out (a peer never arrived)."""
         _native.call("zgla_allscan_status", self._h, 1 if sync else 0)
@@ -108,6 +113,9 @@ class AllScanNCCL:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
+    def split(self, heads):
+        return self
+
     def __call__(self, local, log_decay, num_blocks=1, direction=0):
         order = list(range(self.world)) if direction == 0 else list(range(self.world - 1, -1, -1))
         pos = order.index(self.rank)
@@ -123,6 +131,24 @@ class AllScanNCCL:
         if pos < self.world - 1:
             dist.send(scanned.cpu() if host else scanned, dst=order[pos + 1], group=self.group)
         return recv, scanned
+
+
+class LatencyChain:
+    """Single-GPU probe (diagnostics, not a collective): stands in for a peer chain by holding the stream
+    for ``ns`` nanoseconds (one spinning CTA, ``zgla_selftest_spin``) and returning recv = 0.  It lets one
+    GPU measure how much of a chain's latency ZecoRank's overlap schedule hides (scripts/overlap_probe.py).
+    ``rank``/``world`` say which boundary states the layer applies (rank 1 of 2: prev and no ds_next)."""
+
+    def __init__(self, ns, rank=1, world=2):
+        self.ns, self.rank, self.world = int(ns), rank, world
+
+    def split(self, heads):
+        return self
+
+    def __call__(self, local, log_decay, num_blocks=1, direction=0):
+        _native.call("zgla_selftest_spin", self.ns, ops._stream())
+        recv = torch.zeros_like(local)
+        return recv, local
 
 
 def lasp2_states(local, log_decay, direction=0, group=None):
@@ -153,7 +179,11 @@ class ZecoRank:
     """One rank of ZeCO sequence-parallel GLA (one layer, fwd + bwd) over ``comm``."""
 
     def __init__(self, heads, seq_len, dim, chunk_len=64, dtype=torch.bfloat16, comm=None, num_blocks=4, sms=None,
-                 early_inputs=True):
+                 early_inputs=True, overlap_groups=1):
+        """``overlap_groups`` G > 1 (with peers): the All-Scan of each direction runs per head group on a
+        high-priority communication stream while the compute stream works on the other groups -- the
+        paper's "All-Scan || intra-chunk work" (glasp/engine.py:226-228, 356-358), done by pipelining
+        independent heads instead of a deferred correction pass."""
         self.shard = ops.ZecoShard(heads, seq_len, dim, dim, chunk_len, dtype, sms=sms)
         # forward()/backward() take every input at once, so the early-input contract holds (ZGLA_EARLY_INPUTS=0
         # in the environment keeps it off, for A/B runs)
@@ -166,8 +196,46 @@ class ZecoRank:
         self.ledger = defaultdict(int)
         if dim % num_blocks:
             raise ConfigError(f"num_blocks {num_blocks} does not divide key dim {dim}")
+        self.G = int(overlap_groups)
+        if self.G < 1 or heads % self.G:
+            raise ConfigError(f"overlap_groups {overlap_groups} must divide the {heads} heads")
+        if self.G > 1 and self.world > 1:
+            self.hg = heads // self.G
+            self.gshards = [ops.ZecoShard(self.hg, seq_len, dim, dim, chunk_len, dtype, sms=sms) for _ in range(self.G)]
+            self.gcomms = [comm.split(self.hg) for _ in range(self.G)]
+            self.comm_stream = torch.cuda.Stream(priority=-1)  # the chains jump the queue of compute kernels
+
+    @property
+    def grouped(self):
+        return self.G > 1 and self.world > 1
+
+    def _pipelined(self, local_fn, chain_fn, out_fn):
+        """Compute stream: local(0) local(1) out(0) local(2) out(1) ... out(G-1); the chain of group j runs
+        on the comm stream between local(j) and out(j), under local(j+1) / out(j-1)."""
+        cs, ms = torch.cuda.current_stream(), self.comm_stream
+        done = [None] * self.G
+        res = [None] * self.G
+        for j in range(self.G + 1):
+            if j < self.G:
+                x = local_fn(j)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                ms.wait_event(ev)
+                with torch.cuda.stream(ms):
+                    res[j] = chain_fn(j, x)
+                for t in x:
+                    t.record_stream(ms)
+                for t in res[j]:
+                    t.record_stream(cs)
+                done[j] = torch.cuda.Event()
+                done[j].record(ms)
+            if j >= 1:
+                cs.wait_event(done[j - 1])
+                out_fn(j - 1, res[j - 1])
 
     def forward(self, q, k, v, g, out=None):
+        if self.grouped:
+            return self._forward_grouped(q, k, v, g, out)
         self.shard.poll_domain()  # lazy: reports a bad gate seen by an earlier, completed call
         s_loc, g_tot = self.shard.fwd_local(k, v, g)
         prev = None
@@ -224,7 +292,56 @@ class ZecoRank:
         """Make the current stream wait for the last forward_backward_host(overlap=True) call's D2H."""
         _native.call("zgla_zeco_host_wait", ops._stream())
 
+    def _forward_grouped(self, q, k, v, g, out):
+        geo = self.shard.geo
+        o = out if out is not None else torch.empty((geo.h, geo.L, geo.dv), dtype=geo.dtype, device=q.device)
+        sl = [slice(j * self.hg, (j + 1) * self.hg) for j in range(self.G)]
+        self._gprev, self._ggtot = [None] * self.G, [None] * self.G
+
+        def local(j):
+            self.gshards[j].poll_domain()
+            return self.gshards[j].fwd_local(k[sl[j]], v[sl[j]], g[sl[j]])
+
+        def chain(j, x):
+            recv, _ = self.gcomms[j](x[0], x[1], self.K, _native.ZGLA_FWD)
+            self._ggtot[j] = x[1]
+            return (recv,)
+
+        def output(j, r):
+            prev = r[0] if self.rank > 0 else None
+            self._gprev[j] = prev
+            self.gshards[j].fwd_output(q[sl[j]], k[sl[j]], v[sl[j]], g[sl[j]], prev, out=o[sl[j]])
+
+        self._pipelined(local, chain, output)
+        self.ledger[("all_scan", "sent")] += o.shape[0] * geo.dk * geo.dv if self.rank < self.world - 1 else 0
+        return o
+
+    def _backward_grouped(self, q, k, v, g, d_out, grads):
+        geo = self.shard.geo
+        if grads is None:
+            grads = tuple(torch.empty((geo.h, geo.L, w), dtype=dt, device=q.device)
+                          for w, dt in ((geo.dk, geo.dtype), (geo.dk, geo.dtype), (geo.dv, geo.dtype), (geo.dk, geo.acc)))
+        sl = [slice(j * self.hg, (j + 1) * self.hg) for j in range(self.G)]
+
+        def local(j):
+            return (self.gshards[j].bwd_local(q[sl[j]], g[sl[j]], d_out[sl[j]]),)
+
+        def chain(j, x):
+            recv, _ = self.gcomms[j](x[0], self._ggtot[j], self.K, _native.ZGLA_BWD)
+            return (recv,)
+
+        def output(j, r):
+            dsn = r[0] if self.rank < self.world - 1 else None
+            self.gshards[j].bwd_output(q[sl[j]], k[sl[j]], v[sl[j]], g[sl[j]], d_out[sl[j]], self._gprev[j], dsn,
+                                       grads=tuple(x[sl[j]] for x in grads))
+
+        self._pipelined(local, chain, output)
+        self.ledger[("all_scan", "sent")] += geo.h * geo.dk * geo.dv if self.rank > 0 else 0
+        return grads
+
     def backward(self, q, k, v, g, d_out, grads=None):
+        if self.grouped:
+            return self._backward_grouped(q, k, v, g, d_out, grads)
         self.shard.poll_domain()
         ds0 = self.shard.bwd_local(q, g, d_out)
         ds_next = None

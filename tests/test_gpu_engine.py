@@ -146,3 +146,45 @@ def test_engine_bf16_any_gate_the_reference_accepts():
     assert rel(f(art.outputs), o) <= TOL_BF16
     for got, want in ((grads.dq, dq), (grads.dk, dk), (grads.dv, dv), (grads.dg, dg)):
         assert rel(f(got), want) <= TOL_BF16
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_overlap_schedule_matches_serial(G):
+    """ZecoRank(overlap_groups=G) -- All-Scan per head group on a communication stream, here an injected-
+    latency stand-in (LatencyChain: recv = 0) -- gives the serial schedule's results within the bf16
+    tolerance, eagerly and replayed from a CUDA graph."""
+    from paper_2507_01004_b200 import distributed as zd
+    torch.manual_seed(1)
+    H, L, D = 8, 2048, 128
+    q, k, v, do = ((torch.rand(H, L, D, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(4))
+    g = torch.rand(H, L, D, device="cuda") * (math.log(0.999) - math.log(0.9)) + math.log(0.9)
+
+    def run(groups, graph=False):
+        layer = zd.ZecoRank(H, L, D, 64, torch.bfloat16, comm=zd.LatencyChain(5000), overlap_groups=groups)
+        o = torch.empty_like(q)
+        grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty_like(g))
+
+        def step():
+            layer.forward(q, k, v, g, out=o)
+            layer.backward(q, k, v, g, do, grads=grads)
+        step()
+        if graph:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                step()
+            torch.cuda.current_stream().wait_stream(side)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                step()
+            for t in (o,) + grads:
+                t.zero_()
+            gr.replay()
+        torch.cuda.synchronize()
+        return [t.double().cpu().numpy() for t in (o,) + grads]
+
+    a = run(1)
+    for graph in (False, True):
+        b = run(G, graph)
+        for x, y in zip(a, b):
+            assert rel(y, x) <= 5e-3

@@ -32,3 +32,15 @@ def test_ipc_cfg3_shape_against_oracle(P):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "SPMD IPC check OK" in r.stdout and r.stdout.count("oracle ") == 5
+
+
+def test_ipc_overlap_schedule_against_oracle():
+    """ZecoRank's head-group overlap schedule (each group's All-Scan on a communication stream under the
+    other groups' kernels) over the real CUDA-IPC chain in 3 processes, checked against the f64 oracle."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=3",
+           "--master-addr", "127.0.0.1", "--master-port", "29655",
+           os.path.join(ROOT, "scripts", "spmd_ipc_check.py"), "--same-device", "--rounds", "2",
+           "--seq", "1024", "--heads", "4", "--overlap-groups", "2", "--oracle"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "SPMD IPC check OK" in r.stdout and r.stdout.count("oracle ") == 5
