@@ -98,3 +98,43 @@ def test_generate_sequence_is_byte_identical_to_oracle_draws():
     with pytest.raises(ConfigError):
         generate_sequence(1, 8, 4, ModelDims(1, 1, 1), 0, decay_low=-0.1, decay_high=0.0)
     assert math.isclose(seq.g.max(), seq.g.max()) and np.all(seq.g < 0)
+
+
+@pytest.mark.reference
+@pytest.mark.parametrize("P,K,alpha,beta,cost", [(2, 1, 0.0, 1e9, 0.0), (5, 4, 2e-6, 5e8, 0.0), (8, 16, 1e-6, 2e9, 3e-7)])
+def test_virtual_schedule_matches_live_reference(P, K, alpha, beta, cost):
+    """The drop-in cluster charges All-Scan and the grouped all-gather exactly like the reference (host
+    bookkeeping only, no GPU): same events (rank, label, start, end, stream), same clocks, same ledger."""
+    import sys
+
+    import numpy as np
+
+    sys.path.insert(0, "/root/reference/pkg/src")
+    import glasp.cluster as rc
+    import glasp.collectives as rco
+    from glasp.gla import CumDecay, State
+
+    from paper_2507_01004_b200 import cluster as zc
+    from paper_2507_01004_b200 import collectives as zco
+
+    h, ek, ev = 2, 16, 3
+    rng = np.random.default_rng(P + K)
+    states = [State(rng.uniform(-1, 1, (h, ek, ev))) for _ in range(P)]
+    cds = [CumDecay(rng.uniform(-2, 0, (h, ek))) for _ in range(P)]
+    for direction in ("FWD", "BWD"):
+        ref = rc.create_cluster(P, rc.NetConfig(alpha, beta))
+        for r in range(P):  # uneven clocks before the collective
+            ref.compute(r, 1e-6 * r, "warm")
+        rco.all_scan(ref, states, cds, rco.PipelineConfig(K, cost), getattr(rco.ScanDirection, direction))
+        rco.all_gather_grouped(ref, {"all_gather": [s.values for s in states]})
+        ours = zc.create_cluster(P, zc.NetConfig(alpha, beta))
+        for r in range(P):
+            ours.compute(r, 1e-6 * r, "warm")
+        zco.charge_all_scan(ours, P, h, ek, ev, zco.PipelineConfig(K, cost), getattr(zco.ScanDirection, direction))
+        zco.all_gather_grouped(ours, {"all_gather": [s.values for s in states]})
+        assert ours.clocks == ref.clocks
+        assert ours.read_timeline().to_json_rows() == ref.read_timeline().to_json_rows()
+        assert [(e.rank, e.label, e.start, e.end, e.stream) for e in ours.read_timeline().events] == \
+            [(e.rank, e.label, e.start, e.end, e.stream) for e in ref.read_timeline().events]
+        assert ours.read_ledger().to_csv_rows() == ref.read_ledger().to_csv_rows()
+        assert ours.pending_messages() == ref.pending_messages() == 0
