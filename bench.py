@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--blocks", type=int, default=4, help="All-Scan pipeline blocks K")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-variants", action="store_true", help="skip the extra H=32 x d=64 line item")
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--e2e-groups", type=int, default=4, help="head groups of the host-buffer pipeline")
     p.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
@@ -383,6 +384,51 @@ def collective_bench(comm, H, D, K, dev, rank, world, same_device, barrier, max_
     return res
 
 
+def variant_step(H, L, D, C, seed, dev, steps):
+    """ms per fwd+bwd step (CUDA graph; inputs larger than L2) of another head geometry."""
+    import torch
+    from paper_2507_01004_b200 import distributed as zd
+    gen = torch.Generator(device=dev).manual_seed(seed * 1000 + 7)
+
+    def uni(lo, hi, dt):
+        return (torch.rand((H, L, D), device=dev, generator=gen) * (hi - lo) + lo).to(dt)
+    q, k, v, do = (uni(-1, 1, torch.bfloat16) for _ in range(4))
+    g = uni(math.log(0.9), math.log(0.999), torch.float32)
+    layer = zd.ZecoRank(H, L, D, C, torch.bfloat16)
+    o = torch.empty_like(q)
+    grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty_like(g))
+
+    def step():
+        layer.forward(q, k, v, g, out=o)
+        layer.backward(q, k, v, g, do, grads=grads)
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        step()
+    torch.cuda.current_stream().wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        graph.replay()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    fwd_b, bwd_b = bytes_per_token_head(D, D)
+    hbm, _, _ = peaks()
+    return {"heads": H, "head_dim": D, "tokens": L, "ms_per_step": ms, "tokens_per_s": L / (ms / 1e3),
+            "fast_path": "head pairs" if D == 64 and H % 2 == 0 else "d=128",
+            "hbm_frac_step": (fwd_b + bwd_b) * H * L / (ms / 1e3) / 1e9 / hbm}
+
+
 # ------------------------------------------------------------------ GPU arm
 
 def main():
@@ -594,6 +640,10 @@ def main():
         line["allscan"] = collective_bench(comm, H, D, args.blocks, dev, rank, world, args.same_device,
                                            dist.barrier, max_over_ranks)
 
+    if world == 1 and not args.no_variants and (H, D) == (16, 128):
+        # the same token count as the paper's GLA-1B heads (32 x 64, BASELINE config 1's head size): the
+        # d = 64 head-pair kernels, graph-timed the same way (an extra line item, not the headline)
+        line["variants"] = {"h32_d64": variant_step(32, L, 64, C, args.seed, dev, args.steps)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_legs(H, D, C, 1024, 3, "repeat (3 repeats)")
     if rank == 0:
