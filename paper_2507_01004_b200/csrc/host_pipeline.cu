@@ -56,20 +56,9 @@ static int get_ctx(Ctx** out, size_t nev) {
   return ZGLA_OK;
 }
 
-// the five transfers of one group and direction: one batched submission (ZGLA_COPY_BATCH=0: five copies)
+// the five transfers of one group and direction: one cudaMemcpyAsync each (each tensor's group slice is
+// contiguous, so five large copies per group and direction)
 static int copy5(void** dsts, void** srcs, size_t* sizes, cudaMemcpyKind kind, cudaStream_t st) {
-  static const bool batch = [] {
-    const char* e = std::getenv("ZGLA_COPY_BATCH");
-    return !(e && e[0] == '0');
-  }();
-  if (batch) {
-    cudaMemcpyAttributes attr = {};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t idx = 0, fail = 0;
-    if (cudaMemcpyBatchAsync(dsts, srcs, sizes, 5, &attr, &idx, 1, &fail, st) == cudaSuccess) return ZGLA_OK;
-    cudaGetLastError();  // fall back to individual copies
-  }
   for (int i = 0; i < 5; ++i)
     if (cudaError_t r = cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], kind, st)) return cuda_fail(r, "host copy");
   return ZGLA_OK;
