@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
     bwd_out_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                    const __grid_constant__ CUtensorMap tm_sp, const __grid_constant__ CUtensorMap tm_g,
-                   const float* __restrict__ g, long long gts, long long ghs, long long L, int in3d, int dr,
+                   const __grid_constant__ CUtensorMap tm_dg, const float* __restrict__ g, long long gts, long long ghs, long long L, int in3d, int dr,
                    int nseg,
                    int ntiles, const float* __restrict__ Sin, const float* __restrict__ cumG,
                    const float* __restrict__ dS, const float* __restrict__ gamseg, const float* __restrict__ s_prev,
@@ -515,6 +515,10 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const float gam_c = vgam[st * D + c], r_c = vr[st * D + c];
       if (m > 0) mbar_wait(qdo_full, (m - 1) & 1);
       tc_fence_after();
+      if constexpr (DENSE && ZGLA_DG_TMA) {  // dp_buf staged the previous tile's dg: its bulk store has read it
+        if (tid == 0) tma_store_wait_read0();
+        named_bar(3, 256);
+      }
       {
         const float f = fast_exp(gam_c - r_c + r_next);
         uint8_t* dst = dp_buf + (PAIR ? he : ch) * SPANEL;  // D' [c][v]: PAIR writes the head's diagonal block
@@ -598,17 +602,44 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       const float rho_end = xr[c];
       const float t_upper = xcarry[D + c], t_lower = xcarry[c];
       float base = rho_end + (ch == 0 ? t_lower + t_upper : t_upper);
-      float* pdg = dg + oh * gs.gh + tok0 * gs.gt + oc;
+      if constexpr (DENSE && ZGLA_DG_TMA) {
+        // dg rows -> the D' buffer (free from grads_full until the next tile's rescale) as fp32 [token][channel]
+        // (PAIR: one [64][64] block per head), then one bulk tensor store per head: whole-wavefront STS instead
+        // of 32 scalar global stores per thread
+        float* stg = reinterpret_cast<float*>(dp_buf) + (PAIR ? he * (T * 64) + cols * 64 + oc : cols * D + c);
 #pragma unroll
-      for (int i = 0; i < 32; ++i, pdg += gs.gt) {
-        if (DENSE || PAIR || c < dr) *pdg = base;
-        base -= da[i];
+        for (int i = 0; i < 32; ++i) {
+          stg[i * DW] = base;
+          base -= da[i];
+        }
+        fence_proxy_async();
+        if (tid == 0) ZTRACE(tr, 9, m);
+        named_bar(2, 256);  // staging complete; everyone has read xr / xcarry of this tile
+        if (tid == 0) {
+          if constexpr (PAIR) {
+            tma_store_2d(&tm_dg, dp_buf, 0, (int)((2 * hh) * L + (long long)n * T));
+            tma_store_2d(&tm_dg, dp_buf + T * 64 * 4, 0, (int)((2 * hh + 1) * L + (long long)n * T));
+          } else {
+            tma_store_2d(&tm_dg, dp_buf, 0, (int)(hh * L + (long long)n * T));
+          }
+          tma_store_commit();
+        }
+      } else {
+        float* pdg = dg + oh * gs.gh + tok0 * gs.gt + oc;
+#pragma unroll
+        for (int i = 0; i < 32; ++i, pdg += gs.gt) {
+          if (DENSE || PAIR || c < dr) *pdg = base;
+          base -= da[i];
+        }
+        if (tid == 0) ZTRACE(tr, 9, m);
+        named_bar(2, 256);  // everyone has read xr / xcarry of this tile
       }
-      if (tid == 0) ZTRACE(tr, 9, m);
-      named_bar(2, 256);  // everyone has read xr / xcarry of this tile
       if (ch == 0) xr[c] = rho_end + t_lower + t_upper;  // rho at the start of this tile
     }
     if (nt > 0) mbar_wait(qdo_full, (nt - 1) & 1);  // last Dt accumulation retired before dealloc
+    if constexpr (DENSE && ZGLA_DG_TMA) {
+      if (tid == 0) tma_store_wait0();  // the last dg store has left shared memory (and completed)
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -639,9 +670,12 @@ int fast_bwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
     const bool dn = is_dense64(g, pl.L) && is_dense64(dq, pl.L) && is_dense64(dk, pl.L) && is_dense64(dv, pl.L) &&
                     is_dense64(dg, pl.L);
     auto kern = dn ? bwd_out_kernel<true, true> : bwd_out_kernel<false, true>;
+    CUtensorMap mdg = mg;  // dense: fp32 [2h * L][64], one [64 tokens][64 channels] box per head
+    if (dn && ZGLA_DG_TMA)
+      if (int rc = make_map(&mdg, dg.p, false, (unsigned long long)heads * pl.L, 64, 64, T, false)) return rc;
     set_smem_once((const void*)kern, (int)BO_SMEM);
     if (cudaError_t e = launch_kp(pdl_enabled(), kern, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp,
-                                  mg, (const float*)g.p, g.ts, g.hs, pl.L, 1, 64, pl.nseg, pl.ntiles,
+                                  mg, mdg, (const float*)g.p, g.ts, g.hs, pl.L, 1, 64, pl.nseg, pl.ntiles,
                                   (const float*)w.Sin, (const float*)w.cumG, (const float*)w.dS, (const float*)w.gam,
                                   (const float*)s_prev, (const float*)w.Dend, (const float*)w.cumGr,
                                   (const float*)ds_next, (__nv_bfloat16*)dq.p, (__nv_bfloat16*)dk.p,
@@ -660,9 +694,12 @@ int fast_bwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   if (int rc = map_gate(&mg, g, pl.L, pl.h, din && is_dense(g, pl.L))) return rc;
   const Strides4 gs{(int)dq.ts, (int)dk.ts, (int)dv.ts, (int)dg.ts, dq.hs, dk.hs, dv.hs, dg.hs};
   auto kern = dn ? bwd_out_kernel<true> : bwd_out_kernel<false>;
+  CUtensorMap mdg = mg;  // dense: fp32 [h * L][128], one [64 tokens][128 channels] box per tile
+  if (dn && ZGLA_DG_TMA)
+    if (int rc = make_map(&mdg, dg.p, false, (unsigned long long)pl.h * pl.L, D, D, T, false)) return rc;
   set_smem_once((const void*)kern, (int)BO_SMEM);
   if (cudaError_t e = launch_kp(pdl_enabled(), kern, pl.h * pl.nseg, BO_THREADS, BO_SMEM, st, mq, mk, mv, mdo, msp, mg,
-                                (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
+                                mdg, (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
                                 (const float*)w.Sin, (const float*)w.cumG, (const float*)w.dS, (const float*)w.gam, (const float*)s_prev,
                                 (const float*)w.Dend, (const float*)w.cumGr, (const float*)ds_next,
                                 (__nv_bfloat16*)dq.p, (__nv_bfloat16*)dk.p, (__nv_bfloat16*)dv.p, (float*)dg.p, gs,

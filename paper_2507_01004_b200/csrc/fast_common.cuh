@@ -29,6 +29,9 @@
 #ifndef ZGLA_O_TMA
 #define ZGLA_O_TMA 1  // fwd: O through a swizzled staging tile and bulk tensor stores (dense outputs)
 #endif
+#ifndef ZGLA_DG_TMA
+#define ZGLA_DG_TMA 1  // bwd: dg staged in the free D' buffer and written with bulk tensor stores (dense outputs)
+#endif
 #ifndef ZGLA_CONSUMER_EVICT_FIRST
 #define ZGLA_CONSUMER_EVICT_FIRST 0  // consumer kernels (K3 / K6): 1 = evict-first hint, 0 = plain loads
 #endif
