@@ -564,8 +564,22 @@ def main():
     value = world * L / (ms_step / 1e3)
 
     # ---- end to end through the C-ABI with pinned HOST buffers (copies inside the timed region)
-    host_in = [x.cpu().pin_memory() for x in (q, k, v, g, do)]
-    host_out = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (o,) + grads]
+    # pinned host tensors carved from one staging arena each way (q k v dO g / o dq dk dv dg back to back,
+    # as a loader filling a pinned staging area would lay them out): the host call then moves each head
+    # group's equal-sized tensors with one 2-D copy
+    def arena(tensors):
+        sizes = [x.numel() * x.element_size() for x in tensors]
+        offs = [0]
+        for b in sizes[:-1]:
+            offs.append(offs[-1] + (b + 255) // 256 * 256)
+        buf = torch.empty(offs[-1] + sizes[-1], dtype=torch.uint8, pin_memory=True)
+        return [buf[o:o + b].view(x.dtype).view(x.shape) for o, b, x in zip(offs, sizes, tensors)]
+
+    hq, hk, hv, hdo, hg = arena([q, k, v, do, g])
+    for h_, d_ in ((hq, q), (hk, k), (hv, v), (hdo, do), (hg, g)):
+        h_.copy_(d_)
+    host_in = [hq, hk, hv, hg, hdo]
+    host_out = arena([o, *grads])
     h2d = sum(x.numel() * x.element_size() for x in host_in)
     d2h = sum(x.numel() * x.element_size() for x in host_out)
 

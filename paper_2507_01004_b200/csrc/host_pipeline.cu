@@ -56,11 +56,46 @@ static int get_ctx(Ctx** out, size_t nev) {
   return ZGLA_OK;
 }
 
-// the five transfers of one group and direction: one cudaMemcpyAsync each (each tensor's group slice is
-// contiguous, so five large copies per group and direction)
-static int copy5(void** dsts, void** srcs, size_t* sizes, cudaMemcpyKind kind, cudaStream_t st) {
-  for (int i = 0; i < 5; ++i)
-    if (cudaError_t r = cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], kind, st)) return cuda_fail(r, "host copy");
+// the five transfers of one group and direction, in the order given by `ord`: runs of equal-sized
+// transfers whose sources and destinations are both equally spaced (tensors allocated back to back, as
+// the device layout places q k v dO and o dq dk dv) go out as ONE cudaMemcpy2DAsync (rows = tensors), the
+// rest as one cudaMemcpyAsync each.  Each submitted copy costs ~50 us of duplex DMA efficiency on this link,
+// so fewer, larger submissions win.
+static int copy5(void** dsts, void** srcs, size_t* sizes, const int* ord, cudaMemcpyKind kind, cudaStream_t st) {
+  int i = 0;
+  while (i < 5) {
+    const int a = ord[i];
+    int n = 1;
+    long long dp = 0, sp = 0;
+    if (i + 1 < 5) {
+      const int b = ord[i + 1];
+      dp = (long long)((char*)dsts[b] - (char*)dsts[a]);
+      sp = (long long)((char*)srcs[b] - (char*)srcs[a]);
+      if (sizes[b] == sizes[a] && dp >= (long long)sizes[a] && sp >= (long long)sizes[a]) {
+        n = 2;
+        while (i + n < 5) {
+          const int c = ord[i + n], p = ord[i + n - 1];
+          if (sizes[c] != sizes[a] || (char*)dsts[c] - (char*)dsts[p] != dp || (char*)srcs[c] - (char*)srcs[p] != sp)
+            break;
+          ++n;
+        }
+      }
+    }
+    if (sizes[a] == 0) {
+      i += n;
+      continue;
+    }
+    cudaError_t r = n > 1 ? cudaMemcpy2DAsync(dsts[a], (size_t)dp, srcs[a], (size_t)sp, sizes[a], (size_t)n, kind, st)
+                          : cudaMemcpyAsync(dsts[a], srcs[a], sizes[a], kind, st);
+    if (r != cudaSuccess) {  // e.g. a pitch beyond the device limit: one copy per tensor
+      cudaGetLastError();
+      for (int j = 0; j < n; ++j) {
+        const int c = ord[i + j];
+        if (cudaError_t e = cudaMemcpyAsync(dsts[c], srcs[c], sizes[c], kind, st)) return cuda_fail(e, "host copy");
+      }
+    }
+    i += n;
+  }
   return ZGLA_OK;
 }
 
@@ -100,7 +135,7 @@ static int layout(const zgla_shape* s, int num_sms, int groups, bool tapered, La
   const long long out_bytes[5] = {HL * s->value_dim * e, HL * s->key_dim * e, HL * s->key_dim * e,
                                   HL * s->value_dim * e, HL * s->key_dim * a};  // o dq dk dv dg
   long long off = 0;
-  for (int i = 0; i < 5; ++i) lo->in[i] = off, off += al256(in_bytes[i]);
+  for (int i : {0, 1, 2, 4, 3}) lo->in[i] = off, off += al256(in_bytes[i]);  // q k v dO g: equal pitch for 2-D copies
   for (int i = 0; i < 5; ++i) lo->out[i] = off, off += al256(out_bytes[i]);
   long long ws = 0;
   int hmax = 0;
@@ -210,7 +245,8 @@ extern "C" int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head
         srcs[i] = const_cast<unsigned char*>(reinterpret_cast<const unsigned char*>(hin[i])) + h0 * ph_in[i];
         sizes[i] = (size_t)(hg * ph_in[i]);
       }
-      if (int rc = copy5(dsts, srcs, sizes, cudaMemcpyHostToDevice, cx->h2d)) return rc;
+      static const int ord_in[5] = {0, 1, 2, 4, 3};  // q k v dO g
+      if (int rc = copy5(dsts, srcs, sizes, ord_in, cudaMemcpyHostToDevice, cx->h2d)) return rc;
     }
     cudaEventRecord(ev_in[j], cx->h2d);
     if (trace) cudaEventRecord(tev[3 * j], cx->h2d);
@@ -258,7 +294,8 @@ extern "C" int zgla_zeco_fwd_bwd_host(const zgla_shape* s, int num_sms, int head
         srcs[i] = base + lo.out[i] + h0 * ph_out[i];
         sizes[i] = (size_t)(hg * ph_out[i]);
       }
-      if (int rc = copy5(dsts, srcs, sizes, cudaMemcpyDeviceToHost, cx->d2h)) return rc;
+      static const int ord_out[5] = {0, 1, 2, 3, 4};  // o dq dk dv dg
+      if (int rc = copy5(dsts, srcs, sizes, ord_out, cudaMemcpyDeviceToHost, cx->d2h)) return rc;
     }
     cudaEventRecord(ev_d2h[j], cx->d2h);
     if (trace) cudaEventRecord(tev[3 * j + 2], cx->d2h);

@@ -8,7 +8,7 @@ if [ "$1" = "--tests" ]; then TESTS=$2; shift 2; fi
 for rep in 1 2 3; do
   for v in new "$@"; do
     if [ $v = new ]; then L=""; else L="ZGLA_LIB=var/$v/libzeco_gla.so"; fi
-    env $L python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-variants --e2e-steps 2 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err
+    env $L python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-variants --e2e-steps ${E2E_STEPS:-2} > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err
     python -c "import json; d=json.load(open('gpurun_out/ab_$v.json')); print('$v', 'ms/step', round(d['ms_per_step'],4), d['phase_ms'], 'e2e', round(d['e2e']['ms_per_step'],3))" || tail -3 gpurun_out/ab_$v.err
   done
 done

@@ -128,3 +128,37 @@ def test_host_call_d64_vs_oracle():
     for name, a, b in zip(("o", "dq", "dk", "dv", "dg"), out, [want_o] + list(want_g)):
         err = rel(a.double().numpy(), b)
         assert err <= TOL_BF16, f"{name}: rel err {err:.3e}"
+
+
+def _arena(tensors, gap=256):
+    """pinned tensors carved back to back from one buffer (equal pitch for equal sizes): the layout whose
+    equal-sized head-group slices the host call moves with one 2-D copy per direction"""
+    sizes = [x.numel() * x.element_size() for x in tensors]
+    offs = [0]
+    for b in sizes[:-1]:
+        offs.append(offs[-1] + (b + gap - 1) // gap * gap)
+    buf = torch.empty(offs[-1] + sizes[-1], dtype=torch.uint8).pin_memory()
+    out = [buf[o:o + b].view(x.dtype).view(x.shape) for o, b, x in zip(offs, sizes, tensors)]
+    for a, x in zip(out, tensors):
+        a.copy_(x)
+    return out
+
+
+@pytest.mark.parametrize("groups,h", [(1, 4), (2, 4), (4, 7)])
+def test_host_call_arena_layout_bitwise(groups, h):
+    """inputs q k v dO g and outputs o dq dk dv dg carved from one pinned arena each (2-D copies of the
+    equal-sized tensors) give bit-identical results to separate pinned buffers (one copy per tensor)"""
+    from paper_2507_01004_b200 import distributed as zd
+    L, D, dt = 512, 128, torch.bfloat16
+    host = _case(h, L, D, dt)
+    layer = zd.ZecoRank(h, L, D, 64, dt)
+    out_sep = _outs(h, L, D, dt)
+    layer.forward_backward_host(host, out_sep, head_groups=groups)
+    torch.cuda.current_stream().synchronize()
+    q, k, v, g, do = host
+    aq, ak, av, ado, ag = _arena([q, k, v, do, g])
+    out_ar = _arena([torch.zeros_like(x) for x in out_sep])
+    layer.forward_backward_host([aq, ak, av, ag, ado], out_ar, head_groups=groups)
+    torch.cuda.current_stream().synchronize()
+    for name, a, b in zip(("o", "dq", "dk", "dv", "dg"), out_ar, out_sep):
+        assert torch.equal(a, b), name
