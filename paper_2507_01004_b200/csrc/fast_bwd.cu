@@ -145,7 +145,9 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   // under a programmatic (PDL) launch every warp waits for the preceding grid before touching memory;
   // early inputs: only the epilogue warps, whose prologue reads the preceding scan's outputs (Dend, cumGr)
   pdl_trigger();
-  if (!early || warp < 8) pdl_wait();  // early: the other warps stream inputs the preceding kernel did not write
+  // early inputs: no warp waits here; the TMA lane waits before its first S' load, the epilogue warps after
+  // reading the forward's segment states (everything they read before it was written >= 2 grids back)
+  if (!early) pdl_wait();
 
   if (warp == 12) {
     // ---------------- TMA producer (tiles right to left)
@@ -431,14 +433,38 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
     constexpr int NHF = PAIR ? 1 : 2;                            // 32-column halves held per thread
     {
       const long long sidx = (long long)(hh * nseg + s) * D * D + c;  // column-major workspace states
-      const float cgr = ds_next ? expf(cumGr[(hh * nseg + s) * D + c]) : 0.f;
       const float cg = s_prev ? expf(cumG[(hh * nseg + s) * D + c]) : 0.f;
       const float eg = expf(gamseg[(hh * nseg + s) * D + c]);
       // API states are [h][dr][dr]; PAIR: head 2*hh + he, row c % 64
       const long long pidx = PAIR ? ((long long)(2 * hh + he) * 64 + (c & 63)) * 64 + 32 * ch
                                   : ((long long)hh * dr + c) * dr + 64 * ch;
+      // (1) fp32 forward state at the segment end, e^{gam_s} S_in + dS_s: the forward's outputs (complete
+      //     when this grid starts, see fwd/bwd launch order), so with early inputs this overlaps the
+      //     preceding scan / All-Scan grid; explicit FMAs: the same rounding in every kernel variant
+      float se[NHF][32];
+#pragma unroll
+      for (int hf = 0; hf < NHF; ++hf)
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const int jj = 32 * hf + j;
+          const long long o = sidx + (long long)(vcol0 + jj) * D;
+          float4 si = make_float4(Sin[o], Sin[o + D], Sin[o + 2 * D], Sin[o + 3 * D]);
+          const float4 ds = make_float4(dS[o], dS[o + D], dS[o + 2 * D], dS[o + 3 * D]);
+          const bool inb = PAIR || (c < dr && 64 * ch + jj < dr);
+          if (s_prev && inb) {
+            const float4 a = *reinterpret_cast<const float4*>(s_prev + pidx + jj);
+            si.x = fmaf(cg, a.x, si.x); si.y = fmaf(cg, a.y, si.y);
+            si.z = fmaf(cg, a.z, si.z); si.w = fmaf(cg, a.w, si.w);
+          }
+          se[hf][j] = fmaf(eg, si.x, ds.x);
+          se[hf][j + 1] = fmaf(eg, si.y, ds.y);
+          se[hf][j + 2] = fmaf(eg, si.z, ds.z);
+          se[hf][j + 3] = fmaf(eg, si.w, ds.w);
+        }
+      if (early) pdl_wait();  // (2) the cotangent comes from the preceding scan / All-Scan grids
+      const float cgr = ds_next ? expf(cumGr[(hh * nseg + s) * D + c]) : 0.f;
       float rho = 0.f;
-#pragma unroll 1
+#pragma unroll
       for (int hf = 0; hf < NHF; ++hf) {
         float dv32[32];
 #pragma unroll
@@ -446,26 +472,17 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           const int jj = 32 * hf + j;
           const long long o = sidx + (long long)(vcol0 + jj) * D;
           float4 dd = make_float4(Dend[o], Dend[o + D], Dend[o + 2 * D], Dend[o + 3 * D]);
-          float4 si = make_float4(Sin[o], Sin[o + D], Sin[o + 2 * D], Sin[o + 3 * D]);
-          const float4 ds = make_float4(dS[o], dS[o + D], dS[o + 2 * D], dS[o + 3 * D]);
           const bool inb = PAIR || (c < dr && 64 * ch + jj < dr);
           if (ds_next && inb) {
             const float4 a = *reinterpret_cast<const float4*>(ds_next + pidx + jj);
             dd.x = fmaf(cgr, a.x, dd.x); dd.y = fmaf(cgr, a.y, dd.y);
             dd.z = fmaf(cgr, a.z, dd.z); dd.w = fmaf(cgr, a.w, dd.w);
           }
-          if (s_prev && inb) {
-            const float4 a = *reinterpret_cast<const float4*>(s_prev + pidx + jj);
-            si.x = fmaf(cg, a.x, si.x); si.y = fmaf(cg, a.y, si.y);
-            si.z = fmaf(cg, a.z, si.z); si.w = fmaf(cg, a.w, si.w);
-          }
           dv32[j] = dd.x; dv32[j + 1] = dd.y; dv32[j + 2] = dd.z; dv32[j + 3] = dd.w;
-          // fp32 forward state at the segment end: e^{gam_s} S_in + dS_s
-          // explicit FMAs: the same rounding in every kernel variant
-          rho = fmaf(fmaf(eg, si.x, ds.x), dd.x, rho);
-          rho = fmaf(fmaf(eg, si.y, ds.y), dd.y, rho);
-          rho = fmaf(fmaf(eg, si.z, ds.z), dd.z, rho);
-          rho = fmaf(fmaf(eg, si.w, ds.w), dd.w, rho);
+          rho = fmaf(se[hf][j], dd.x, rho);
+          rho = fmaf(se[hf][j + 1], dd.y, rho);
+          rho = fmaf(se[hf][j + 2], dd.z, rho);
+          rho = fmaf(se[hf][j + 3], dd.w, rho);
         }
         tmem_st32(d_addr + 32 * hf, dv32);  // Dt at the segment end (frame r = 0)
       }
