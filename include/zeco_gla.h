@@ -217,6 +217,8 @@ int zgla_selftest_mma(const void* a, const void* b, float* d, int M, int N, int 
                       int lane_off, void* stream);
 /* diagnostics: one CTA spinning for ns nanoseconds on the stream (injected-latency probes) */
 int zgla_selftest_spin(long long ns, void* stream);
+/* diagnostic: tcgen05 SS MMA issue rate, M x N x 16 bf16; out[cta] = SM milli-cycles per MMA */
+int zgla_selftest_mma_rate(int M, int N, int a_mn, int b_mn, int iters, int ctas, long long* out, void* stream);
 
 #ifdef __cplusplus
 }

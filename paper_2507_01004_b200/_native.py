@@ -100,6 +100,7 @@ _SIGS = {
     "zgla_selftest_stream": ([_P, _LL, _I, _I, _I, _I, _I, _P], _I),
     "zgla_selftest_mma": ([_P, _P, _P, _I, _I, _I, _I, _I, _I, _P], _I),
     "zgla_selftest_spin": ([_LL, _P], _I),
+    "zgla_selftest_mma_rate": ([_I, _I, _I, _I, _I, _I, _P, _P], _I),
 }
 
 EXPORTED = tuple(_SIGS)

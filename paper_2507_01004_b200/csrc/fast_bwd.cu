@@ -29,6 +29,9 @@
 namespace zgla {
 namespace fast {
 
+#ifndef ZGLA_ABL_PART2
+#define ZGLA_ABL_PART2 0  // timing ablation only (wrong results): skip the D'-dependent dk / dv MMAs
+#endif
 constexpr int BO_NS = 2;
 constexpr int BO_STAGE = 4 * TILE_BF16;  // q, k, v, dO
 constexpr int BO_THREADS = 448;          // 8 state warps, 4 prep warps, TMA warp, MMA warp
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           mbar_wait(dp_ready, m & 1);  // D' in smem and Dt rescaled in TMEM
           tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {  // dk^T += D' V^T ; dv^T += D'^T Kh^T
+          for (int kk = 0; kk < (ZGLA_ABL_PART2 ? 0 : D / 16); ++kk) {  // dk^T += D' V^T ; dv^T += D'^T Kh^T
             const uint32_t boff = (kk >> 2) * PANEL + (kk & 3) * 32;
             mma_bf16_ss(tbase + BC_DK, sdesc(dpa + (kk >> 2) * SPANEL + (kk & 3) * 32, 16, 1024),
                         sdesc(va + boff, 16, 1024), id_kk, 1);

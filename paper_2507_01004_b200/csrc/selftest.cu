@@ -246,3 +246,71 @@ extern "C" int zgla_selftest_spin(long long ns, void* stream) {
   selftest_spin_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ns);
   return zgla_check_launch();
 }
+
+// ---------------------------------------------------------------------------
+// Diagnostic: tcgen05 MMA issue rate.  Every CTA (one per SM) issues `iters` groups of 8 SS MMAs of shape
+// M x N x 16 (bf16, operands in SW128 shared memory, contents irrelevant) into one TMEM accumulator,
+// commits each group to an mbarrier and waits for the last; out[blockIdx.x] = SM cycles per MMA.
+namespace zgla {
+template <bool TS>
+__global__ void __launch_bounds__(128) selftest_mma_rate_kernel(int M, int N, int a_mn, int b_mn, int iters,
+                                                                long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 131072 / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async();
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (tid < 32) {
+    tmem_alloc(&tmem_base_sh, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base_sh;
+  if (tid == 0) {
+    const uint32_t idesc = idesc_bf16(M, N, a_mn != 0, b_mn != 0);
+    const uint32_t sa = smem_u32(smem), sb = sa + 65536;  // MN-major panels 16 KiB apart
+    uint64_t ad[4], bd[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      ad[kk] = a_mn ? sdesc(sa + kk * 2048, 16384, 1024) : sdesc(sa + kk * 32, 16, 1024);
+      bd[kk] = b_mn ? sdesc(sb + kk * 2048, 16384, 1024) : sdesc(sb + kk * 32, 16, 1024);
+    }
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if constexpr (TS)
+          mma_bf16_ts(tbase, tbase + 256 + (kk & 3) * 8, bd[kk & 3], idesc, 1u);
+        else
+          mma_bf16_ss(tbase, ad[kk & 3], bd[kk & 3], idesc, 1u);
+      }
+      mma_commit(&bar);
+    }
+    mbar_wait(&bar, (iters - 1) & 1);
+    const long long t1 = clock64();
+    out[blockIdx.x] = (t1 - t0) * 1000 / (8ll * iters);  // milli-cycles per MMA
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tmem_dealloc(tbase, 512);
+}
+}  // namespace zgla
+
+extern "C" int zgla_selftest_mma_rate(int M, int N, int a_mn, int b_mn, int iters, int ctas, long long* out,
+                                      void* stream) {
+  using namespace zgla;
+  if (!((M == 64 || M == 128) && N % 16 == 0 && N >= 16 && N <= 256 && iters > 0 && ctas > 0)) return ZGLA_ERR_DIMS;
+  const size_t smem = 1024 + 131072;
+  auto kern = a_mn == 2 ? selftest_mma_rate_kernel<true> : selftest_mma_rate_kernel<false>;  // 2: A from TMEM
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<ctas, 128, smem, (cudaStream_t)stream>>>(M, N, a_mn == 2 ? 0 : a_mn, b_mn, iters, out);
+  return zgla_check_launch();
+}
