@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-variants", action="store_true", help="skip the extra H=32 x d=64 line item")
     p.add_argument("--e2e-steps", type=int, default=5)
-    p.add_argument("--e2e-groups", type=int, default=4, help="head groups of the host-buffer pipeline")
+    p.add_argument("--e2e-groups", type=int, default=2, help="head groups of the host-buffer pipeline")
     p.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     p.add_argument("--same-device", action="store_true",
                    help="validation only: all ranks on cuda:0 with a gloo bootstrap (timings meaningless)")
