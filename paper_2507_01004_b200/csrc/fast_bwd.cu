@@ -29,6 +29,9 @@
 namespace zgla {
 namespace fast {
 
+#ifndef ZGLA_RHO_RESEED
+#define ZGLA_RHO_RESEED 8  // tiles between dg re-seeds from rowsum(S' (.) Dt) (0: never)
+#endif
 #ifndef ZGLA_ABL_PART2
 #define ZGLA_ABL_PART2 0  // timing ablation only (wrong results): skip the D'-dependent dk / dv MMAs
 #endif
@@ -54,6 +57,12 @@ constexpr uint32_t BC_DQ = 0, BC_DK = 64, BC_DV = 128, BC_QDO = 192, BC_SC = 320
 constexpr uint32_t BC_SC2 = 256;
 __device__ __forceinline__ int pair_channel(int lane_id) {  // TMEM lane (0..127) -> channel of the pair
   return 64 * ((lane_id & 31) >> 4) + 16 * (lane_id >> 5) + (lane_id & 15);
+}
+
+// dg re-seeding (section 4 of DESIGN.md): on tile m with (m + 1) % ZGLA_RHO_RESEED == 0 the seed of the next
+// tile is rho_n = rowsum(S'_n (.) Dt_n); k-th such tile -> parity k & 1 of the sp_read barrier
+__device__ __forceinline__ bool reseed_tile(int m, int nt) {
+  return ZGLA_RHO_RESEED > 0 && m + 1 < nt && (m + 1) % (ZGLA_RHO_RESEED > 0 ? ZGLA_RHO_RESEED : 1) == 0;
 }
 
 template <bool DENSE, bool PAIR = false>
@@ -97,6 +106,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   uint64_t* sp_empty = sc_full + 8;
   uint64_t* lb_empty = sc_full + 9;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sc_full + 11);
+  uint64_t* sp_read = sc_full + 12;  // dg re-seed tiles: the epilogue has read S' (the producer may reload it)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int hh = blockIdx.x / nseg, s = blockIdx.x % nseg;
@@ -129,6 +139,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
     mbar_init(sp_empty, 1);
     mbar_init(&lb_empty[0], 256);
     mbar_init(&lb_empty[1], 256);
+    mbar_init(sp_read, 256);
     fence_barrier_init();
   }
   uint8_t* am1_buf = sp_buf + T * 128;  // PAIR: S' panel 0 rows 64-127
@@ -190,6 +201,8 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         // for the preceding grid (whose completion implies every earlier one's) before its first S' load
         if (m == 0 && early) pdl_wait();
         mbar_wait(sp_empty, (m & 1) ^ 1);
+        if (m > 0 && reseed_tile(m - 1, nt))  // the previous S' also fed the epilogue's dg re-seed
+          mbar_wait(sp_read, ((m / (ZGLA_RHO_RESEED > 0 ? ZGLA_RHO_RESEED : 1)) - 1) & 1);
         if constexpr (PAIR) {  // the two per-head blocks onto the diagonal of the [c][v] buffer
           mbar_arrive_expect_tx(sp_full, 2 * T * 128);
           tma_load_2d(sp_buf, &tm_sp, sp_full, 0, ((2 * hh) * ntiles + n) * 64);
@@ -571,6 +584,35 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
       mbar_wait(grads_full, m & 1);
       tc_fence_after();
       if (tid == 0) ZTRACE(tr, 8, m);
+      const bool reseed = reseed_tile(m, nt);
+      if (reseed) {
+        // the suffix sum of da beyond this tile's start from the state identity rho_n = rowsum(S_n (.) D_n) =
+        // rowsum(S'_n (.) Dt_n) (both in this tile's frame; Dt_n after this tile's accumulation), so the bf16
+        // error of da does not accumulate along long segments.  The producer holds the next S' load until
+        // this read (sp_read).
+        mbar_wait(sp_full, m & 1);
+        mbar_wait(qdo_full, m & 1);
+        tc_fence_after();
+        const uint8_t* srow = sp_buf + (PAIR ? he : ch) * SPANEL;
+        float part = 0.f;
+#pragma unroll 1
+        for (int hf = 0; hf < NHF; ++hf) {
+          float x[32];
+          tmem_ld32(d_addr + 32 * hf, x);
+#pragma unroll
+          for (int mm = 0; mm < 4; ++mm) {
+            const uint4 w = *reinterpret_cast<const uint4*>(srow + sw128(c, (PAIR ? 4 * ch : 4 * hf) + mm));
+            const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              part = fmaf(__uint_as_float(wv[u] << 16), x[8 * mm + 2 * u], part);
+              part = fmaf(__uint_as_float(wv[u] & 0xffff0000u), x[8 * mm + 2 * u + 1], part);
+            }
+          }
+        }
+        mbar_arrive(sp_read);
+        xrho[ch * D + c] = part;
+      }
       const uint8_t* sb = smem + st * BO_STAGE;
       const uint32_t cols = 32 * ch;
       const uint32_t lbcol = BC_LB + 64 * (m & 1) + cols;
@@ -654,7 +696,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
         if (tid == 0) ZTRACE(tr, 9, m);
         named_bar(2, 256);  // everyone has read xr / xcarry of this tile
       }
-      if (ch == 0) xr[c] = rho_end + t_lower + t_upper;  // rho at the start of this tile
+      if (ch == 0) xr[c] = reseed ? xrho[c] + xrho[D + c] : rho_end + t_lower + t_upper;  // rho at this tile's start
     }
     if (nt > 0) mbar_wait(qdo_full, (nt - 1) & 1);  // last Dt accumulation retired before dealloc
     if constexpr (DENSE && ZGLA_DG_TMA) {

@@ -337,3 +337,54 @@ def test_chunk_scalings_against_oracle(dtype):
         assert got.dtype == dtype and rel(got, w) <= tol
     np.testing.assert_allclose(cs.decay_from_start * cs.decay_to_end,
                                np.broadcast_to(cs.chunk_decay[:, None, :], gch.shape), rtol=1e-5 if dtype == np.float32 else 1e-14)
+
+
+def _shard_step(q, k, v, g, do, dtype):
+    """one P = 1 fwd + bwd through the per-rank entry points in `dtype` (bf16: fused tcgen05 kernels;
+    fp32: the SIMT kernels with the exact token recurrence inside each chunk)"""
+    from paper_2507_01004_b200 import ops
+    h, L, D = q.shape
+    sh = ops.ZecoShard(h, L, D, D, 64, dtype)
+    assert sh.fast == (dtype == torch.bfloat16)
+    Q, K_, V, DO = (x.to(dtype) for x in (q, k, v, do))
+    sh.fwd_local(K_, V, g)
+    o = sh.fwd_output(Q, K_, V, g, None)
+    sh.bwd_local(Q, g, DO)
+    grads = sh.bwd_output(Q, K_, V, g, DO, None, None)
+    torch.cuda.synchronize()
+    return [o.double().cpu().numpy()] + [x.double().cpu().numpy() for x in grads]
+
+
+def test_fast_single_tile_shard():
+    """L = 64: one tile, one segment per head (the smallest shard the fused path takes)"""
+    q, k, v, g, do = make_case(3, 1, 64, seed=5, long_memory=True)
+    got = run_fast(q, k, v, g, do, 1)
+    check(got, oracle(q, k, v, g, do, 1))
+
+
+def test_fast_long_shard_against_fp32_kernels():
+    """BASELINE config 5's per-GPU length (131,072 tokens, 2,048 tiles per head, 228-tile segments): the fused
+    bf16 path against the fp32 SIMT path on the same (bf16-rounded) inputs, both gate distributions"""
+    h, L, D = 2, 131072, 128
+    gen = torch.Generator(device="cuda").manual_seed(17)
+    u = lambda lo, hi: torch.rand((h, L, D), device="cuda", generator=gen) * (hi - lo) + lo  # noqa: E731
+    q, k, v, do = (u(-1, 1).to(torch.bfloat16).float() for _ in range(4))
+    for lo, hi in ((orc.DECAY_LOW, orc.DECAY_HIGH), (orc.LONG_DECAY_LOW, orc.LONG_DECAY_HIGH)):
+        g = u(lo, hi).float()
+        a = _shard_step(q, k, v, g, do, torch.bfloat16)
+        b = _shard_step(q, k, v, g, do, torch.float32)
+        errs = {name: rel(x, y) for name, x, y in zip(("o", "dq", "dk", "dv", "dg"), a, b)}
+        print("long shard rel errors", {n: f"{e:.2e}" for n, e in errs.items()})
+        assert all(e <= TOL_BF16 for e in errs.values()), errs
+
+
+@pytest.mark.parametrize("sms", [1, 4])
+def test_fast_dg_long_segments_default_gates(sms):
+    """dg = suffix sum of da: without re-seeding, the bf16 error of da accumulates along a segment (one
+    256-tile segment: 2.7e-2 relative before the re-seed, over the 1e-2 bound).  The backward re-seeds the
+    running sum every ZGLA_RHO_RESEED tiles from rowsum(S' (.) Dt), so the error no longer grows with the
+    segment length (one head, 16K tokens, strongly decaying reference gates)"""
+    q, k, v, g, do = make_case(1, 1, 16384, seed=5)
+    got = run_fast(q, k, v, g, do, 1, sms=sms)
+    errs = check(got, oracle(q, k, v, g, do, 1))
+    assert errs["dg"] <= 7e-3, errs
