@@ -378,13 +378,13 @@ def test_fast_long_shard_against_fp32_kernels():
         assert all(e <= TOL_BF16 for e in errs.values()), errs
 
 
-@pytest.mark.parametrize("sms", [1, 4])
-def test_fast_dg_long_segments_default_gates(sms):
+@pytest.mark.parametrize("sms,h,D", [(1, 1, 128), (4, 1, 128), (1, 2, 64), (2, 3, 64)])
+def test_fast_dg_long_segments_default_gates(sms, h, D):
     """dg = suffix sum of da: without re-seeding, the bf16 error of da accumulates along a segment (one
     256-tile segment: 2.7e-2 relative before the re-seed, over the 1e-2 bound).  The backward re-seeds the
     running sum every ZGLA_RHO_RESEED tiles from rowsum(S' (.) Dt), so the error no longer grows with the
     segment length (one head, 16K tokens, strongly decaying reference gates)"""
-    q, k, v, g, do = make_case(1, 1, 16384, seed=5)
+    q, k, v, g, do = make_case(h, 1, 16384, seed=5, D=D)  # d = 64: head pairs (h even) / zero-filled (h odd)
     got = run_fast(q, k, v, g, do, 1, sms=sms)
     errs = check(got, oracle(q, k, v, g, do, 1))
     assert errs["dg"] <= 7e-3, errs
