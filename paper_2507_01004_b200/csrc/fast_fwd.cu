@@ -21,6 +21,9 @@
 #include <vector>
 #include "fast_common.cuh"
 
+#ifndef ZGLA_ABL_NOSCAN
+#define ZGLA_ABL_NOSCAN 0  // timing ablation only (wrong results): skip the segment scans K2 / K5
+#endif
 namespace zgla {
 namespace fast {
 
@@ -825,6 +828,7 @@ int fast_fwd_local(const zgla_shape* s, int num_sms, const TRef& k, const TRef& 
   Ws w = carve(pl, ws);
   if (int rc = launch_seg_state(0, pl, k, v, g, w.dS, w.gam, w.flags, st, domain_sink_of(ws))) return rc;
   const long long n = (long long)pl.h * D * D;
+  if (ZGLA_ABL_NOSCAN) return zgla_check_launch();  // timing ablation only
   if (cudaError_t e = launch_k(seg_scan_kernel<0>, (unsigned)((n / 4 + 127) / 128), 128, 0, st, pl.h, pl.nseg, k.dr,
                                 (const float*)w.dS, (const float*)w.gam, w.Sin, w.cumG, (float*)s_local, (float*)g_tot,
                                 (const float*)nullptr, (const float*)nullptr, pl.pair))
@@ -887,6 +891,7 @@ int fast_bwd_local(const zgla_shape* s, int num_sms, const TRef& q, const TRef& 
   Ws w = carve(pl, ws);
   if (int rc = launch_seg_state(1, pl, q, d_out, g, w.dD, w.gam, nullptr, st)) return rc;
   const long long n = (long long)pl.h * D * D;
+  if (ZGLA_ABL_NOSCAN) return zgla_check_launch();  // timing ablation only
   if (cudaError_t e = launch_k(seg_scan_kernel<1>, (unsigned)((n / 4 + 127) / 128), 128, 0, st, pl.h, pl.nseg, q.dr,
                                 (const float*)w.dD, (const float*)w.gam, w.Dend, w.cumGr, (float*)ds0, (float*)nullptr,
                                 (const float*)w.Sin, (const float*)w.dS, pl.pair))
