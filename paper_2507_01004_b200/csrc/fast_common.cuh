@@ -123,7 +123,18 @@ inline Plan make_plan(const zgla_shape* s, int num_sms) {
 }
 
 // ---- host: TMA descriptors via the driver entry point (no libcuda link dependency)
+// The driver call needs a current context in the calling thread.  A thread that has not touched the runtime
+// yet (e.g. torch's autograd worker running a backward first) has none, and the encode fails with
+// CUDA_ERROR_INVALID_CONTEXT: bind the device's primary context once per thread (cudaFree(0)).
+inline void bind_context_once() {
+  static thread_local bool bound = false;
+  if (!bound) {
+    cudaFree(nullptr);
+    bound = true;
+  }
+}
 inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  bind_context_once();
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
     void* ptr = nullptr;
