@@ -903,9 +903,37 @@ int fast_bwd_local(const zgla_shape* s, int num_sms, const TRef& q, const TRef& 
 
 namespace zgla {
 // ---- lazy domain reports: workspace -> host-mapped flag word (zgla_zeco_watch_domain)
+// Words come from slabs of host-mapped memory allocated once and never freed: a cudaHostAlloc /
+// cudaFreeHost per shard would cost milliseconds and synchronise the device (cudaFreeHost does) every
+// time a short-lived shard (one per layer call) comes and goes.  A released word is reused only after
+// kQuarantine later releases, so a segment pass still in flight cannot mark its next owner.
 namespace {
 std::mutex g_dom_mu;
 std::unordered_map<const void*, std::pair<int*, int*>> g_dom;  // ws -> (host, device) pointers
+constexpr int kSlab = 4096, kQuarantine = 1024;
+std::vector<std::pair<int*, int*>> g_dom_free;                  // never used
+std::vector<std::pair<int*, int*>> g_dom_released;              // FIFO of released words
+size_t g_dom_released_head = 0;
+int take_word(std::pair<int*, int*>* out) {
+  if (g_dom_released.size() - g_dom_released_head > (size_t)kQuarantine) {
+    *out = g_dom_released[g_dom_released_head++];
+    if (g_dom_released_head > 4096) {  // compact the consumed prefix now and then
+      g_dom_released.erase(g_dom_released.begin(), g_dom_released.begin() + (long)g_dom_released_head);
+      g_dom_released_head = 0;
+    }
+    return ZGLA_OK;
+  }
+  if (g_dom_free.empty()) {
+    int* h = nullptr;
+    int* d = nullptr;
+    if (cudaError_t e = cudaHostAlloc(&h, kSlab * sizeof(int), cudaHostAllocMapped)) return cuda_fail(e, "cudaHostAlloc");
+    if (cudaError_t e = cudaHostGetDevicePointer(&d, h, 0)) return cuda_fail(e, "cudaHostGetDevicePointer");
+    for (int i = kSlab - 1; i >= 0; --i) g_dom_free.emplace_back(h + i, d + i);
+  }
+  *out = g_dom_free.back();
+  g_dom_free.pop_back();
+  return ZGLA_OK;
+}
 }  // namespace
 int* domain_sink_of(const void* ws) {
   std::lock_guard<std::mutex> lock(g_dom_mu);
@@ -916,12 +944,10 @@ int watch_domain(const void* ws, int** host_flag) {
   std::lock_guard<std::mutex> lock(g_dom_mu);
   auto it = g_dom.find(ws);
   if (it == g_dom.end()) {
-    int* h = nullptr;
-    int* d = nullptr;
-    if (cudaError_t e = cudaHostAlloc(&h, sizeof(int), cudaHostAllocMapped)) return cuda_fail(e, "cudaHostAlloc");
-    *h = 0;
-    if (cudaError_t e = cudaHostGetDevicePointer(&d, h, 0)) return cuda_fail(e, "cudaHostGetDevicePointer");
-    it = g_dom.emplace(ws, std::make_pair(h, d)).first;
+    std::pair<int*, int*> w;
+    if (int rc = take_word(&w)) return rc;
+    *w.first = 0;
+    it = g_dom.emplace(ws, w).first;
   }
   if (host_flag) *host_flag = it->second.first;
   return ZGLA_OK;
@@ -930,7 +956,7 @@ int unwatch_domain(const void* ws) {
   std::lock_guard<std::mutex> lock(g_dom_mu);
   auto it = g_dom.find(ws);
   if (it != g_dom.end()) {
-    cudaFreeHost(it->second.first);
+    g_dom_released.push_back(it->second);
     g_dom.erase(it);
   }
   return ZGLA_OK;

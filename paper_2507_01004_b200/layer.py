@@ -47,7 +47,7 @@ class ZecoGLAFunction(torch.autograd.Function):
         dv = v.shape[2]
         # strided [h, L, d] views (e.g. head slices of token-major projections) are read in place
         q, k, v, g = (x if x.stride(2) == 1 else x.contiguous() for x in (q, k, v, g))
-        shard = ops.ZecoShard(h, L, dk, dv, chunk_len, q.dtype, device=q.device)
+        shard = ops.ZecoShard(h, L, dk, dv, chunk_len, q.dtype, device=q.device, watch_domain=False)
         s_loc, g_tot = shard.fwd_local(k, v, g)
         prev = None
         world = comm.world if comm is not None else 1

@@ -281,9 +281,11 @@ class ZecoShard:
     four ZeCO entry points of the C ABI.
     """
 
-    def __init__(self, heads, seq_len, key_dim, value_dim, chunk_len, dtype, device=None, sms=None, ws=None):
+    def __init__(self, heads, seq_len, key_dim, value_dim, chunk_len, dtype, device=None, sms=None, ws=None,
+                 watch_domain=True):
         """``ws``: adopt an existing workspace (e.g. one saved for backward by an autograd Function) instead
-        of allocating one; such a shard does not register the lazy domain watch."""
+        of allocating one; such a shard does not register the lazy domain watch.  ``watch_domain=False``
+        skips the watch for shards nobody polls (one per layer call)."""
         self.geo = Geometry(heads, seq_len, key_dim, value_dim, chunk_len, dtype)
         self.shape = self.geo.shape()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -296,7 +298,7 @@ class ZecoShard:
         self.ws = _ws(nbytes, self.device) if ws is None else ws
         self.fast = bool(_native.load().zgla_fast_path(ctypes.byref(self.shape)))
         self._dom = None
-        if self.fast and ws is None:  # lazy domain reports of the fused forward segment pass (host-mapped word)
+        if self.fast and ws is None and watch_domain:  # lazy domain reports of the fused segment pass (host-mapped word)
             dom = ctypes.POINTER(ctypes.c_int)()
             _native.call("zgla_zeco_watch_domain", _p(self.ws), ctypes.byref(dom))
             self._dom = dom

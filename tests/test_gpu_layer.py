@@ -106,3 +106,13 @@ def test_layer_d64_heads_strided_plumbing():
     for a, b in zip(outs[0][2], outs[1][2]):
         assert rel(a, b) <= 1e-6
     assert rel(outs[0][0], outs[2][0]) <= TOL_BF16
+
+
+def test_layer_shards_do_not_watch_the_domain():
+    """The layer builds one shard per call and never polls it: no host-mapped domain word per call (a
+    cudaHostAlloc / cudaFreeHost pair per shard synchronised the device and slowed GLA-1.3B by ~50 %)."""
+    import torch
+    from paper_2507_01004_b200 import ops
+    a = ops.ZecoShard(2, 256, 128, 128, 64, torch.bfloat16, watch_domain=False)
+    b = ops.ZecoShard(2, 256, 128, 128, 64, torch.bfloat16)
+    assert a._dom is None and b._dom is not None
