@@ -44,3 +44,15 @@ def test_ipc_overlap_schedule_against_oracle():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "SPMD IPC check OK" in r.stdout and r.stdout.count("oracle ") == 5
+
+
+@pytest.mark.parametrize("P,D", [(2, 128), (3, 64)])
+def test_ipc_layer_function_against_torch_reference(P, D):
+    """The autograd layer function (the GLAModel path) sequence-parallel over P processes with AllScanP2P,
+    token-major head-slice inputs, outputs and gradients against the float64 torch GLA on the whole sequence."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29671 + P),
+           os.path.join(ROOT, "scripts", "spmd_layer_check.py"), "--same-device", "--seq", "512", "--dim", str(D)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "SPMD layer check OK" in r.stdout, r.stdout[-2000:]
