@@ -246,7 +246,7 @@ class ZecoRank:
         self._prev, self._g_tot = prev, g_tot
         return self.shard.fwd_output(q, k, v, g, prev, out=out)
 
-    def forward_backward_host(self, host_in, host_out, head_groups=4, overlap=False):
+    def forward_backward_host(self, host_in, host_out, head_groups=2, overlap=False):
         """One layer forward + backward with inputs (q, k, v, g, dO) and outputs (o, dq, dk, dv, dg) in
         HOST memory (CPU torch tensors, pinned for full PCIe rate), through the C-ABI call
         ``zgla_zeco_fwd_bwd_host``: heads are pipelined in ``head_groups`` groups so host->device,
