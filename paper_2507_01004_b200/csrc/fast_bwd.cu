@@ -29,6 +29,9 @@
 namespace zgla {
 namespace fast {
 
+#ifndef ZGLA_SP_WAIT
+#define ZGLA_SP_WAIT 0
+#endif
 #ifndef ZGLA_RHO_RESEED
 #define ZGLA_RHO_RESEED 8  // tiles between dg re-seeds from rowsum(S' (.) Dt) (0: never)
 #endif
@@ -197,9 +200,11 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
           tile_load<DENSE>(sb + 3 * TILE_BF16, &tm_do, &full[st], 0, r, hh, L, in3d, pol);
           tile_load<DENSE>(sb + 3 * TILE_BF16 + PANEL, &tm_do, &full[st], 64, r, hh, L, in3d, pol);
         }
-        // S' comes from the forward output kernel three launches back: with early inputs this lane waits
-        // for the preceding grid (whose completion implies every earlier one's) before its first S' load
-        if (m == 0 && early) pdl_wait();
+        // S' comes from the forward output kernel, which has completed when this grid starts in the entry-point
+        // order: every grid between the two (segment pass, segment scan, All-Scan chain) waits for its
+        // predecessor before it lets its dependents launch.  ZGLA_SP_WAIT=1 keeps a wait for the preceding
+        // grid before the first S' load anyway
+        if (ZGLA_SP_WAIT && m == 0 && early) pdl_wait();
         mbar_wait(sp_empty, (m & 1) ^ 1);
         if (m > 0 && reseed_tile(m - 1, nt))  // the previous S' also fed the epilogue's dg re-seed
           mbar_wait(sp_read, ((m / (ZGLA_RHO_RESEED > 0 ? ZGLA_RHO_RESEED : 1)) - 1) & 1);
