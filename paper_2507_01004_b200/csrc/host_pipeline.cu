@@ -15,6 +15,8 @@
 // With a peer communicator (world > 1) every group runs its own All-Scan on
 // the group's [hg, dk, dv] states; all ranks walk the groups in the same
 // order, so the chain protocol's epochs line up.
+#include <cuda.h>
+
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
@@ -61,6 +63,26 @@ static int get_ctx(Ctx** out, size_t nev) {
 // the device layout places q k v dO and o dq dk dv) go out as ONE cudaMemcpy2DAsync (rows = tensors), the
 // rest as one cudaMemcpyAsync each.  Each submitted copy costs ~50 us of duplex DMA efficiency on this link,
 // so fewer, larger submissions win.
+// true iff the byte ranges [a, a+1) and [b, b+1) lie in the same CUDA allocation (pinned host memory or device
+// memory; unified addressing): a 2-D copy may only span rows of one allocation
+static bool same_alloc(const void* a, const void* b) {
+  using Fn = CUresult (*)(void*, CUpointer_attribute, CUdeviceptr);
+  static Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return (cudaGetDriverEntryPoint("cuPointerGetAttribute", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+               ? reinterpret_cast<Fn>(p)
+               : nullptr;
+  }();
+  if (!fn) return false;
+  CUdeviceptr sa = 0, sb = 0;
+  if (fn(&sa, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, reinterpret_cast<CUdeviceptr>(a)) != CUDA_SUCCESS ||
+      fn(&sb, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, reinterpret_cast<CUdeviceptr>(b)) != CUDA_SUCCESS)
+    return false;
+  return sa == sb;
+}
+
 static int copy5(void** dsts, void** srcs, size_t* sizes, const int* ord, cudaMemcpyKind kind, cudaStream_t st) {
   int i = 0;
   while (i < 5) {
@@ -84,6 +106,17 @@ static int copy5(void** dsts, void** srcs, size_t* sizes, const int* ord, cudaMe
     if (sizes[a] == 0) {
       i += n;
       continue;
+    }
+    if (n > 1) {  // the rows must lie in one allocation on both sides (tensors carved from one arena)
+      const int last = ord[i + n - 1];
+      if (!same_alloc(srcs[a], (char*)srcs[last] + sizes[a] - 1) || !same_alloc(dsts[a], (char*)dsts[last] + sizes[a] - 1)) {
+        for (int j = 0; j < n; ++j) {
+          const int c = ord[i + j];
+          if (cudaError_t e = cudaMemcpyAsync(dsts[c], srcs[c], sizes[c], kind, st)) return cuda_fail(e, "host copy");
+        }
+        i += n;
+        continue;
+      }
     }
     cudaError_t r = n > 1 ? cudaMemcpy2DAsync(dsts[a], (size_t)dp, srcs[a], (size_t)sp, sizes[a], (size_t)n, kind, st)
                           : cudaMemcpyAsync(dsts[a], srcs[a], sizes[a], kind, st);
