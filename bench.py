@@ -261,6 +261,36 @@ def cpu_single_process(H, D, C, L, P, K, seed=0):
                       f"{'ZECO K=' + str(K) if P > 1 else 'SINGLE_DEVICE'}, f64, one process"}
 
 
+def cpu_collectives(P=8, H=16, D=128, K=4, reps=3):
+    """Variant: the reference's All-Scan (glasp/collectives.py:70-140) and its all-gather-of-states baseline
+    (all_gather_grouped, glasp/collectives.py:149-174) at BASELINE config 4's 1 MiB-per-rank state, wall
+    clock of the CPU implementation (virtual cluster, one process; best of `reps`)."""
+    if _reference_kind() != "reference":
+        return {"unavailable": "baseline/_ref (the unmodified glasp) is not installed"}
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from glasp.cluster import NetConfig, create_cluster
+    from glasp.collectives import PipelineConfig, ScanDirection, all_gather_grouped, all_scan
+    from glasp.gla import CumDecay, State
+    rng = np.random.default_rng(0)
+    states = [State(rng.uniform(-1, 1, (H, D, D))) for _ in range(P)]
+    decays = [CumDecay(rng.uniform(-2, 0, (H, D))) for _ in range(P)]
+    best_scan = best_ag = float("inf")
+    for _ in range(reps):
+        cl = create_cluster(P, NetConfig())
+        t0 = time.perf_counter()
+        all_scan(cl, states, decays, PipelineConfig(num_blocks=K), ScanDirection.FWD)
+        best_scan = min(best_scan, time.perf_counter() - t0)
+        cl = create_cluster(P, NetConfig())
+        t0 = time.perf_counter()
+        all_gather_grouped(cl, {"s": [x.values for x in states], "g": [x.log_values for x in decays]})
+        best_ag = min(best_ag, time.perf_counter() - t0)
+    return {"all_scan_us": best_scan * 1e6, "all_gather_states_us": best_ag * 1e6, "P": P, "K": K,
+            "state_bytes_per_rank_fp32": H * D * D * 4, "kind": "reference", "processes": 1,
+            "sample": f"unmodified glasp all_scan(FWD, K={K}) / all_gather_grouped over a virtual cluster of {P} "
+                      f"ranks, H={H}, d={D} (f64 arrays), wall clock, best of {reps}"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's own CPU implementation of the path on this box's host cores."""
     if rank != 0:
@@ -292,6 +322,7 @@ def run_reference(args, rank, world):
         "variants": {
             "single_process_cfg2_sample": cpu_single_process(H, D, C, 256, 1, 1),
             "single_process_cfg1": cpu_single_process(4, 64, 64, 2048, 2, 4),
+            "collectives_cfg4": cpu_collectives(),
         },
     }
     print(json.dumps(line), flush=True)
