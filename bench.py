@@ -415,6 +415,42 @@ def collective_bench(comm, H, D, K, dev, rank, world, same_device, barrier, max_
     return res
 
 
+def allscan_virtual(H, D, K, dev, iters=20):
+    import torch
+    from paper_2507_01004_b200 import _native, ops
+    lib = _native.load()
+    out = {"note": "P ranks on one GPU (list-form kernel, LL words through L2), not NVLink; us per call",
+           "state_bytes_per_rank": H * D * D * 4, "K": K}
+    for P in (2, 4, 8):
+        local = torch.rand(P, H, D, D, device=dev)
+        logs = -torch.rand(P, H, D, device=dev)
+        recv, scanned = torch.empty_like(local), torch.empty_like(local)
+
+        def call():
+            _native.check(lib.zgla_allscan_local(P, H, D, D, _native.ZGLA_F32, K, 0, ops._p(local), ops._p(logs),
+                                                 ops._p(recv), ops._p(scanned), ops._stream()), "allscan")
+        for _ in range(3):
+            call()
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            call()
+        torch.cuda.current_stream().wait_stream(side)
+        with torch.cuda.graph(graph):
+            for _ in range(iters):
+                call()
+        graph.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        graph.replay()
+        b.record()
+        torch.cuda.synchronize()
+        out[f"P{P}_us"] = round(a.elapsed_time(b) * 1e3 / iters, 2)
+    return out
+
+
 def variant_step(H, L, D, C, seed, dev, steps):
     """ms per fwd+bwd step (CUDA graph; inputs larger than L2) of another head geometry."""
     import torch
@@ -685,6 +721,11 @@ def main():
         line["allscan"] = collective_bench(comm, H, D, args.blocks, dev, rank, world, args.same_device,
                                            dist.barrier, max_over_ranks)
 
+    if world == 1:
+        # All-Scan microbench in the same run (BASELINE config 4 at this step's state size): P = 2 / 4 / 8 ranks
+        # simulated on this GPU by the list-form kernel (the SPMD kernel's chain code, words through L2, one
+        # launch), graph-timed; the NVLink numbers come from the N > 1 lines
+        line["allscan_virtual"] = allscan_virtual(H, D, args.blocks, dev)
     if world == 1 and not args.no_variants and (H, D) == (16, 128):
         # the same token count as the paper's GLA-1B heads (32 x 64, BASELINE config 1's head size): the
         # d = 64 head-pair kernels, graph-timed the same way (an extra line item, not the headline)
