@@ -91,8 +91,7 @@ __global__ void __launch_bounds__(BO_THREADS, 1)
   float* vgam = reinterpret_cast<float*>(smem + BO_OFF_VEC);
   float* vr = vgam + BO_NS * D;
   float* xrho = reinterpret_cast<float*>(smem + BO_OFF_X + 1024);  // [2][D] row-sum partials
-  float* xtot = xrho + 2 * D;                                      // [D] logb of row 31 (epilogue)
-  float* xcarry = xtot + D;                                        // [2][D] per-half sums of da
+  float* xcarry = xrho + 3 * D;                                    // [2][D] per-half sums of da
   float* xr = xcarry + 2 * D;                                      // [D] rho at the current tile end
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + BO_OFF_BAR);
   uint64_t* full = bars;
