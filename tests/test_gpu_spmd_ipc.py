@@ -56,3 +56,15 @@ def test_ipc_layer_function_against_torch_reference(P, D):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "SPMD layer check OK" in r.stdout, r.stdout[-2000:]
+
+
+def test_ipc_eight_processes_against_oracle():
+    """The north star's P = 8: eight processes over the real CUDA-IPC All-Scan chain (sharing one GPU), bitwise
+    equal to the single-process list form and within the bf16 bound of the f64 oracle."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr", "127.0.0.1", "--master-port", "29701",
+           os.path.join(ROOT, "scripts", "spmd_ipc_check.py"), "--same-device", "--rounds", "2",
+           "--seq", "256", "--heads", "2", "--oracle"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "SPMD IPC check OK (P=8" in r.stdout and r.stdout.count("oracle ") == 5
