@@ -451,6 +451,34 @@ def allscan_virtual(H, D, K, dev, iters=20):
     return out
 
 
+def dropin_cfg1(reps=5):
+    """BASELINE config 1 through the drop-in's reference API exactly as a glasp user calls it (NumPy f64 in and
+    out, run_forward / run_backward(ZECO) with the virtual-cluster bookkeeping): the same call the reference
+    arm's single_process_cfg1 times on the CPU, here on the fp64 CUDA kernels (host copies included)."""
+    import time
+    import torch
+    from paper_2507_01004_b200 import (ModelDims, NetConfig, PipelineConfig, StrategyKind, create_cluster,
+                                       generate_sequence, run_backward, run_forward)
+    P, L, H, D, C, K = 2, 2048, 4, 64, 64, 4
+    seq = generate_sequence(P, L, C, ModelDims(H, D, D), 0)
+    do = np.random.default_rng(1).uniform(-1, 1, (H, P * L, D))
+
+    def call():
+        art = run_forward(seq, StrategyKind.ZECO, create_cluster(P, NetConfig()), PipelineConfig(K))
+        run_backward(seq, do, StrategyKind.ZECO, create_cluster(P, NetConfig()), PipelineConfig(K), art)
+    call()
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        call()
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    return {"value": P * L / best, "unit": UNIT, "seconds": best, "dtype": "f64",
+            "call": "paper_2507_01004_b200.run_forward / run_backward(ZECO), NumPy f64 arrays, P=2 x 2048 tokens, "
+                    "H=4, d=64, K=4 (the reference arm's single_process_cfg1 on the drop-in), best of 5"}
+
+
 def variant_step(H, L, D, C, seed, dev, steps):
     """ms per fwd+bwd step (CUDA graph; inputs larger than L2) of another head geometry."""
     import torch
@@ -729,7 +757,8 @@ def main():
     if world == 1 and not args.no_variants and (H, D) == (16, 128):
         # the same token count as the paper's GLA-1B heads (32 x 64, BASELINE config 1's head size): the
         # d = 64 head-pair kernels, graph-timed the same way (an extra line item, not the headline)
-        line["variants"] = {"h32_d64": variant_step(32, L, 64, C, args.seed, dev, args.steps)}
+        line["variants"] = {"h32_d64": variant_step(32, L, 64, C, args.seed, dev, args.steps),
+                            "dropin_api_cfg1": dropin_cfg1()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_legs(H, D, C, 1024, 3, "repeat (3 repeats)")
     if rank == 0:
