@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libzeco_gla.so")
 
 ZGLA_BF16, ZGLA_F32, ZGLA_F64 = 0, 1, 2
 ZGLA_FWD, ZGLA_BWD = 0, 1
+ZGLA_FWD_NO_SAVE = 1  # zgla_zeco_fwd_output_ex_v flag: skip the chunk-start states the backward reads
 ZGLA_HOST_OVERLAP = 1
 
 _CODES = {
@@ -79,6 +80,7 @@ _SIGS = {
     "zgla_zeco_unwatch_domain": ([_P], _I),
     "zgla_zeco_fwd_local_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _P, _P, _P, _P], _I),
     "zgla_zeco_fwd_output_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _T, _P, _P, _T, _P], _I),
+    "zgla_zeco_fwd_output_ex_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _T, _P, _P, _T, _I, _P], _I),
     "zgla_zeco_bwd_local_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _P, _P, _P], _I),
     "zgla_zeco_bwd_output_v": ([ctypes.POINTER(Shape), _I, _T, _T, _T, _T, _T, _P, _P, _P, _T, _T, _T, _T, _P], _I),
     "zgla_allscan_local": ([_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P], _I),

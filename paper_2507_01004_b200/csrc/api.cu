@@ -59,7 +59,7 @@ long long fast_ws_bytes(const zgla_shape* s, int num_sms);
 int fast_fwd_local(const zgla_shape*, int, const fast::TRef&, const fast::TRef&, const fast::TRef&, void*, void*,
                    void*, cudaStream_t);
 int fast_fwd_output(const zgla_shape*, int, const fast::TRef&, const fast::TRef&, const fast::TRef&,
-                    const fast::TRef&, void*, const void*, const fast::TRef&, cudaStream_t);
+                    const fast::TRef&, void*, const void*, const fast::TRef&, cudaStream_t, bool save_states = true);
 int fast_bwd_local(const zgla_shape*, int, const fast::TRef&, const fast::TRef&, const fast::TRef&, void*, void*,
                    cudaStream_t);
 int fast_bwd_output(const zgla_shape*, int, const fast::TRef&, const fast::TRef&, const fast::TRef&,
@@ -139,14 +139,22 @@ extern "C" int zgla_zeco_fwd_local_v(const zgla_shape* s, int num_sms, const zgl
 extern "C" int zgla_zeco_fwd_output_v(const zgla_shape* s, int num_sms, const zgla_tensor* q, const zgla_tensor* k,
                                       const zgla_tensor* v, const zgla_tensor* g, void* ws, const void* s_prev,
                                       const zgla_tensor* o, void* stream) {
+  return zgla_zeco_fwd_output_ex_v(s, num_sms, q, k, v, g, ws, s_prev, o, 0, stream);
+}
+
+extern "C" int zgla_zeco_fwd_output_ex_v(const zgla_shape* s, int num_sms, const zgla_tensor* q, const zgla_tensor* k,
+                                         const zgla_tensor* v, const zgla_tensor* g, void* ws, const void* s_prev,
+                                         const zgla_tensor* o, int flags, void* stream) {
   if (int rc = validate_zeco(s, num_sms)) return rc;
+  if (flags & ~ZGLA_FWD_NO_SAVE) return ZGLA_ERR_CONFIG;
   const bool fp = fast_supported(s);
   if (int rc = check_refs(s, {q, k, v, g, o}, fp)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const long long L = s->seq_len;
   if (fp)
     return fast_fwd_output(s, num_sms, fast::as_ref(q, L, s->heads, s->key_dim), fast::as_ref(k, L, s->heads, s->key_dim), fast::as_ref(v, L, s->heads, s->key_dim),
-                           fast::as_ref(g, L, s->heads, s->key_dim), ws, s_prev, fast::as_ref(o, L, s->heads, s->key_dim), st);
+                           fast::as_ref(g, L, s->heads, s->key_dim), ws, s_prev, fast::as_ref(o, L, s->heads, s->key_dim), st,
+                           (flags & ZGLA_FWD_NO_SAVE) == 0);
   return generic_zeco_fwd_output(s, q->data, k->data, v->data, g->data, ws, s_prev, o->data, st);
 }
 

@@ -837,7 +837,7 @@ int fast_fwd_local(const zgla_shape* s, int num_sms, const TRef& k, const TRef& 
 }
 
 int fast_fwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef& k, const TRef& v, const TRef& g,
-                    void* ws, const void* s_prev, const TRef& o, cudaStream_t st) {
+                    void* ws, const void* s_prev, const TRef& o, cudaStream_t st, bool save_states) {
   const Plan pl = make_plan(s, num_sms);
   Ws w = carve(pl, ws);
   CUtensorMap mq, mk, mv, mg, msp;
@@ -858,7 +858,7 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
     if (cudaError_t e = launch_kp(pdl_enabled(), kern, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
                                   mo, (const float*)g.p, g.ts, g.hs, pl.L, 1, 64, pl.nseg, pl.ntiles,
                                   (const float*)w.Sin, (const float*)w.cumG, (const float*)s_prev, (__nv_bfloat16*)o.p,
-                                  o.ts, o.hs, w.Sp, g_trace_buf, g_trace_cta, early))
+                                  o.ts, o.hs, save_states ? w.Sp : nullptr, g_trace_buf, g_trace_cta, early))
       return cuda_fail(e, "fwd_out_kernel (pairs)");
     return zgla_check_launch();
   }
@@ -879,7 +879,7 @@ int fast_fwd_output(const zgla_shape* s, int num_sms, const TRef& q, const TRef&
   if (cudaError_t e = launch_kp(pdl_enabled(), kern, pl.h * pl.nseg, FO_THREADS, FO_SMEM, st, mq, mk, mv, mg, msp,
                                 mo, (const float*)g.p, g.ts, g.hs, pl.L, din ? 0 : 1, q.dr, pl.nseg, pl.ntiles,
                                 (const float*)w.Sin, (const float*)w.cumG, (const float*)s_prev, (__nv_bfloat16*)o.p,
-                                o.ts, o.hs, w.Sp,
+                                o.ts, o.hs, save_states ? w.Sp : nullptr,
                                 g_trace_buf, g_trace_cta, early))
     return cuda_fail(e, "fwd_out_kernel");
   return zgla_check_launch();

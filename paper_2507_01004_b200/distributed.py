@@ -233,9 +233,11 @@ class ZecoRank:
                 cs.wait_event(done[j - 1])
                 out_fn(j - 1, res[j - 1])
 
-    def forward(self, q, k, v, g, out=None):
+    def forward(self, q, k, v, g, out=None, save_states=True):
+        """``save_states=False``: forward only (inference / evaluation); skips the chunk-start states the
+        backward reads, and a later backward raises StateError."""
         if self.grouped:
-            return self._forward_grouped(q, k, v, g, out)
+            return self._forward_grouped(q, k, v, g, out, save_states)
         self.shard.poll_domain()  # lazy: reports a bad gate seen by an earlier, completed call
         s_loc, g_tot = self.shard.fwd_local(k, v, g)
         prev = None
@@ -244,7 +246,7 @@ class ZecoRank:
             self.ledger[("all_scan", "sent")] += s_loc.numel() if self.rank < self.world - 1 else 0
             prev = recv if self.rank > 0 else None
         self._prev, self._g_tot = prev, g_tot
-        return self.shard.fwd_output(q, k, v, g, prev, out=out)
+        return self.shard.fwd_output(q, k, v, g, prev, out=out, save_states=save_states)
 
     def forward_backward_host(self, host_in, host_out, head_groups=2, overlap=False):
         """One layer forward + backward with inputs (q, k, v, g, dO) and outputs (o, dq, dk, dv, dg) in
@@ -292,7 +294,7 @@ class ZecoRank:
         """Make the current stream wait for the last forward_backward_host(overlap=True) call's D2H."""
         _native.call("zgla_zeco_host_wait", ops._stream())
 
-    def _forward_grouped(self, q, k, v, g, out):
+    def _forward_grouped(self, q, k, v, g, out, save_states=True):
         geo = self.shard.geo
         o = out if out is not None else torch.empty((geo.h, geo.L, geo.dv), dtype=geo.dtype, device=q.device)
         sl = [slice(j * self.hg, (j + 1) * self.hg) for j in range(self.G)]
@@ -310,7 +312,8 @@ class ZecoRank:
         def output(j, r):
             prev = r[0] if self.rank > 0 else None
             self._gprev[j] = prev
-            self.gshards[j].fwd_output(q[sl[j]], k[sl[j]], v[sl[j]], g[sl[j]], prev, out=o[sl[j]])
+            self.gshards[j].fwd_output(q[sl[j]], k[sl[j]], v[sl[j]], g[sl[j]], prev, out=o[sl[j]],
+                                       save_states=save_states)
 
         self._pipelined(local, chain, output)
         self.ledger[("all_scan", "sent")] += o.shape[0] * geo.dk * geo.dv if self.rank < self.world - 1 else 0

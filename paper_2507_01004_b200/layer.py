@@ -58,7 +58,10 @@ class ZecoGLAFunction(torch.autograd.Function):
         # outputs and gradients are produced token-major ([L, h, d] storage, [h, L, d] views), the layout the
         # surrounding GEMMs consume: the runtime-stride kernel variant costs ~10 % of the core
         # (scripts/strided_bench.py) but saves the transposing copies (GLA-1.3B step 2.06 -> 1.87 s)
-        o = shard.fwd_output(q, k, v, g, prev, out=_token_major(h, L, dv, q.dtype, q.device))
+        # forward-only calls (no input needs a gradient: torch.no_grad() evaluation) skip the chunk-start
+        # states that only the backward reads
+        o = shard.fwd_output(q, k, v, g, prev, out=_token_major(h, L, dv, q.dtype, q.device),
+                             save_states=any(ctx.needs_input_grad[:4]))
         # everything the backward needs goes through save_for_backward -- including the shard's workspace
         # (segment states, saved chunk states) -- so activation checkpointing can drop and regenerate it
         none = torch.empty(0, device=q.device)

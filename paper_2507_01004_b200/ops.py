@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _native
-from .errors import ConfigError, DimsError, DomainError
+from .errors import ConfigError, DimsError, DomainError, StateError
 
 _CODE = {torch.bfloat16: _native.ZGLA_BF16, torch.float32: _native.ZGLA_F32, torch.float64: _native.ZGLA_F64}
 
@@ -359,8 +359,10 @@ class ZecoShard:
         (synchronises; a validation step, not for the timed path)."""
         _native.call("zgla_zeco_domain_check", ctypes.byref(self.shape), self.sms, _p(self.ws), _stream())
 
-    def fwd_output(self, q, k, v, g, s_prev=None, out=None):
-        """outputs [h, L, dv]; ``out`` may be a strided view (e.g. of a token-major [L, h * dv] buffer)."""
+    def fwd_output(self, q, k, v, g, s_prev=None, out=None, save_states=True):
+        """outputs [h, L, dv]; ``out`` may be a strided view (e.g. of a token-major [L, h * dv] buffer).
+        ``save_states=False``: forward only -- the fused path skips the chunk-start states the backward
+        reads (ZGLA_FWD_NO_SAVE), and a later bwd_output raises StateError."""
         geo = self.geo
         q, k, v, g = (self._chk(q, "q", geo.dk), self._chk(k, "k", geo.dk), self._chk(v, "v", geo.dv),
                       self._chk(g, "g", geo.dk))
@@ -368,8 +370,10 @@ class ZecoShard:
             s_prev = self._chk(s_prev, "s_prev", 0)
         o = out if out is not None else torch.empty((geo.h, geo.L, geo.dv), dtype=geo.dtype, device=self.device)
         o_use = self._chk(o, "o", geo.dv)
-        _native.call("zgla_zeco_fwd_output_v", ctypes.byref(self.shape), self.sms, self._ref(q), self._ref(k),
-                     self._ref(v), self._ref(g), _p(self.ws), _p(s_prev), self._ref(o_use), _stream())
+        _native.call("zgla_zeco_fwd_output_ex_v", ctypes.byref(self.shape), self.sms, self._ref(q), self._ref(k),
+                     self._ref(v), self._ref(g), _p(self.ws), _p(s_prev), self._ref(o_use),
+                     0 if save_states else _native.ZGLA_FWD_NO_SAVE, _stream())
+        self._states_saved = bool(save_states) or not self.fast
         if o_use.data_ptr() != o.data_ptr():
             o.copy_(o_use)
         return o
@@ -384,6 +388,8 @@ class ZecoShard:
 
     def bwd_output(self, q, k, v, g, d_out, s_prev=None, ds_next=None, grads=None):
         """(dq, dk, dv, dg) [h, L, .]; ``grads`` may be strided views."""
+        if not getattr(self, "_states_saved", True):
+            raise StateError("bwd_output after a forward run with save_states=False (no saved chunk states)")
         geo = self.geo
         q, k, v, g = (self._chk(q, "q", geo.dk), self._chk(k, "k", geo.dk), self._chk(v, "v", geo.dv),
                       self._chk(g, "g", geo.dk))

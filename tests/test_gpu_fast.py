@@ -388,3 +388,23 @@ def test_fast_dg_long_segments_default_gates(sms, h, D):
     got = run_fast(q, k, v, g, do, 1, sms=sms)
     errs = check(got, oracle(q, k, v, g, do, 1))
     assert errs["dg"] <= 7e-3, errs
+
+
+def test_fast_forward_only_skips_saved_states():
+    """fwd_output(save_states=False) (inference): the same outputs bit for bit, and a backward after it raises
+    StateError instead of reading chunk states that were never written"""
+    from paper_2507_01004_b200 import ops
+    from paper_2507_01004_b200.errors import StateError
+    q, k, v, g, do = make_case(4, 1, 2048, seed=9)
+    dev = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dt)  # noqa: E731
+    Q, K_, V, DO = (dev(x, torch.bfloat16) for x in (q, k, v, do))
+    G = dev(g, torch.float32)
+    sh = ops.ZecoShard(4, 2048, 128, 128, 64, torch.bfloat16)
+    sh.fwd_local(K_, V, G)
+    a = sh.fwd_output(Q, K_, V, G, None).clone()
+    sh.fwd_local(K_, V, G)
+    b = sh.fwd_output(Q, K_, V, G, None, save_states=False)
+    assert torch.equal(a, b)
+    sh.bwd_local(Q, G, DO)
+    with pytest.raises(StateError):
+        sh.bwd_output(Q, K_, V, G, DO, None, None)

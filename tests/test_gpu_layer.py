@@ -116,3 +116,13 @@ def test_layer_shards_do_not_watch_the_domain():
     a = ops.ZecoShard(2, 256, 128, 128, 64, torch.bfloat16, watch_domain=False)
     b = ops.ZecoShard(2, 256, 128, 128, 64, torch.bfloat16)
     assert a._dom is None and b._dom is not None
+
+
+def test_layer_no_grad_forward_matches():
+    """Under torch.no_grad() the layer skips the saved chunk states (forward only); outputs are bit-identical."""
+    from paper_2507_01004_b200.layer import zeco_gla
+    q, k, v, g, _ = _inputs(2, 512, 128, torch.bfloat16)
+    a = zeco_gla(*(x.clone().requires_grad_(True) for x in (q, k, v, g))).detach()
+    with torch.no_grad():
+        b = zeco_gla(q, k, v, g)
+    assert torch.equal(a, b)
